@@ -1,0 +1,118 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY.
+
+ctypes front-end of ``liboracle.so`` — the CPU restatement of nlkit's
+per-system solvers (see nlk_oracle.cpp for the reference file:line map).
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` leg may import this module; it is the checker, never the
+thing measured or shipped.  The product package never imports it.
+
+Parity status: pinned against golden vectors produced by the unmodified
+reference (tests/golden/make_golden.py); DFSane is builder-authored and
+unpinned (the reference has no DFSane).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+ALGS = {"newton-raphson": 0, "trust-region": 1, "broyden": 2, "klement": 3,
+        "dfsane": 4, "newton-backtracking": 5}
+RETCODES = ("Success", "MaxIters", "LineSearchFailed", "LinearSolveFailed",
+            "Stalled", "NonFinite")
+
+_lib = None
+
+
+def build():
+    """Compile liboracle.so with oracle/Makefile (g++, -ffp-contract=off)."""
+    subprocess.run(["make", "-s", "-C", _HERE, "liboracle.so"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        dp = np.ctypeslib.ndpointer(np.float64, flags="C")
+        ip = np.ctypeslib.ndpointer(np.int32, flags="C")
+        i8 = np.ctypeslib.ndpointer(np.int8, flags="C")
+        c_int, c_i64, c_d = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        L.oracle_lookup.argtypes = [ctypes.c_char_p, c_int, ctypes.POINTER(c_int),
+                                    ctypes.POINTER(c_int), ctypes.POINTER(c_int)]
+        L.oracle_residual.argtypes = [c_int, c_int, dp, ctypes.c_void_p, dp]
+        L.oracle_jacobian.argtypes = [c_int, c_int, dp, ctypes.c_void_p, dp]
+        L.oracle_solve_batch.argtypes = [c_int, c_int, c_int, c_i64, dp, ctypes.c_void_p, c_int,
+                                         c_d, c_int, c_int, dp, dp, i8, ip, ip, ip, ip]
+        L.oracle_ddot.restype = c_d
+        L.oracle_ddot.argtypes = [c_int, dp, dp]
+        L.oracle_gemv_A_x.argtypes = [c_int, dp, dp, dp]
+        L.oracle_gemv_AT_x.argtypes = [c_int, dp, dp, dp]
+        L.oracle_getrf.argtypes = [c_int, dp, ip]
+        L.oracle_getrs.argtypes = [c_int, dp, ip, dp]
+        _lib = L
+    return _lib
+
+
+def lookup(problem_id, n=0):
+    h, nn, m = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = lib().oracle_lookup(problem_id.encode(), int(n), ctypes.byref(h), ctypes.byref(nn),
+                             ctypes.byref(m))
+    if rc != 0:
+        raise KeyError(f"oracle: unknown problem {problem_id!r} (n={n}, rc={rc})")
+    return h.value, nn.value, m.value
+
+
+def _pptr(p):
+    return None if p is None else p.ctypes.data_as(ctypes.c_void_p)
+
+
+def residual(problem_id, x, p=None, n=0):
+    h, nn, m = lookup(problem_id, n or len(x))
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    p = None if m == 0 else np.ascontiguousarray(p, dtype=np.float64)
+    f = np.empty(nn)
+    lib().oracle_residual(h, nn, x, _pptr(p), f)
+    return f
+
+
+def jacobian(problem_id, x, p=None, n=0):
+    """Dual-path Jacobian; returns None on NonFiniteValue."""
+    h, nn, m = lookup(problem_id, n or len(x))
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    p = None if m == 0 else np.ascontiguousarray(p, dtype=np.float64)
+    J = np.empty((nn, nn))
+    ok = lib().oracle_jacobian(h, nn, x, _pptr(p), J)
+    return J if ok else None
+
+
+def solve_batch(problem_id, alg, u0, p=None, abstol=1e-8, maxiters=1000, threads=None):
+    """Solve B systems (u0 [B, n], p [B, m]); returns a dict of arrays."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    B, n = u0.shape
+    h, nn, m = lookup(problem_id, n)
+    if m:
+        p = np.ascontiguousarray(p, dtype=np.float64).reshape(B, m)
+    else:
+        p = None
+    out = {
+        "u": np.empty((B, n)), "resid": np.empty(B),
+        "retcode": np.empty(B, np.int8), "nsteps": np.empty(B, np.int32),
+        "nf": np.empty(B, np.int32), "njac": np.empty(B, np.int32),
+        "nlinsolve": np.empty(B, np.int32),
+    }
+    threads = threads or os.cpu_count() or 1
+    rc = lib().oracle_solve_batch(h, n, ALGS[alg], B, u0, _pptr(p), m, float(abstol),
+                                  int(maxiters), int(threads), out["u"], out["resid"],
+                                  out["retcode"], out["nsteps"], out["nf"], out["njac"],
+                                  out["nlinsolve"])
+    if rc != 0:
+        raise RuntimeError(f"oracle_solve_batch failed rc={rc}")
+    return out
