@@ -1,0 +1,117 @@
+/*
+ * nlk_b200.h — C ABI of the B200 batched small-system nonlinear solver.
+ *
+ * This is the drop-in boundary for the reference's per-system solve path
+ * (/root/reference/pkg/src/nlkit).  The reference is pure Python, so its
+ * "interface" is the Python call
+ *     nlkit.solvers.run_preset(name, Problem(residual, u0, params), SolveOptions(abstol, maxiters))
+ *         -> SolveResult(u_star, resid_norm, retcode, stats)
+ * (solvers.py:640-655, core.py:27-91, 158-169); each entry point below names the
+ * reference piece it replaces.  The Python shim paper_2403_16341_b200 binds
+ * these symbols with ctypes (see INTEGRATION.md for the nlkit-side binding).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch or CUDA types cross the boundary
+ *     (streams are passed as void*; NULL = the legacy default stream);
+ *   - batch arrays are structure-of-arrays: u0/u_out are [n][B] (element i of
+ *     system b at i*B + b), p is [m][B];
+ *   - dtype 0 = IEEE binary64 (the reference's arithmetic), 1 = binary32;
+ *   - retcode values are nlkit's RetCode in declaration order
+ *     (core.py:17-24): 0 Success, 1 MaxIters, 2 LineSearchFailed,
+ *     3 LinearSolveFailed, 4 Stalled, 5 NonFinite;
+ *   - per-system numerical failures are NEVER errors (they are retcodes);
+ *     API misuse returns a negative status and sets nlk_last_error().
+ *   - entry points are re-entrant; the registry is immutable; the library keeps
+ *     no pointer after a call returns.
+ */
+#ifndef NLK_B200_H
+#define NLK_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NLK_API __attribute__((visibility("default")))
+#else
+#define NLK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NLK_OK 0
+#define NLK_ERR_UNKNOWN_PROBLEM (-1)  /* KeyError in problems.get_problem (problems.py:459,474) */
+#define NLK_ERR_BAD_SIZE (-2)         /* n not compiled for this problem */
+#define NLK_ERR_UNKNOWN_ALG (-3)      /* KeyError in run_preset (solvers.py:649-650) */
+#define NLK_ERR_BAD_OPTIONS (-4)      /* ValueError in SolveOptions (core.py:61-65) */
+#define NLK_ERR_BAD_ARGUMENT (-5)     /* null buffer, negative B, missing params */
+#define NLK_ERR_NOT_COMPILED (-6)     /* (problem, n, alg, dtype) has no kernel */
+#define NLK_ERR_CUDA (-7)             /* CUDA runtime error (message in nlk_last_error) */
+
+/* algorithm ids; names match ALGORITHM_PRESETS (solvers.py:610-637) */
+#define NLK_ALG_NEWTON_RAPHSON 0     /* "newton-raphson"      = SimpleNewtonRaphson */
+#define NLK_ALG_TRUST_REGION 1       /* "trust-region"        = SimpleTrustRegion   */
+#define NLK_ALG_BROYDEN 2            /* "broyden"             = SimpleBroyden       */
+#define NLK_ALG_KLEMENT 3            /* "klement"             = SimpleKlement       */
+#define NLK_ALG_DFSANE 4             /* "dfsane"              = SimpleDFSane (no nlkit counterpart) */
+#define NLK_ALG_NEWTON_BACKTRACKING 5 /* "newton-backtracking" (solvers.py:613) */
+
+#define NLK_F64 0
+#define NLK_F32 1
+
+/* Library version (major*10000 + minor*100 + patch). */
+NLK_API int nlk_version(void);
+
+/* Message of the last failed call on this thread ("" if none). */
+NLK_API const char* nlk_last_error(void);
+
+/* Resolve a preset name to an algorithm id (replaces the ALGORITHM_PRESETS
+ * lookup in run_preset, solvers.py:649-651).  Returns NLK_ERR_UNKNOWN_ALG
+ * for names without a batched kernel. */
+NLK_API int nlk_alg_lookup(const char* name);
+
+/* Number of compiled (problem, n) instances and their description. */
+NLK_API int nlk_num_problems(void);
+NLK_API int nlk_problem_info(int32_t handle, const char** id, int32_t* n, int32_t* m);
+
+/* Resolve an nlkit problem id (problems.py:450-474 naming: "test23/<name>",
+ * "quadratic", "generalized_rosenbrock") at size n (0 = the problem's fixed
+ * size).  Replaces binding Problem.residual to a Python callable
+ * (core.py:35): the residual is a compiled device function. */
+NLK_API int nlk_problem_lookup(const char* id, int32_t n, int32_t* handle, int32_t* n_out, int32_t* m_out);
+
+/* Solve B independent systems already resident on the current device.
+ * Replaces B calls of run_preset(alg, Problem(residual, u0_b, p_b),
+ * SolveOptions(abstol, maxiters)) (solvers.py:640-655): writes u_star
+ * (u_out), resid_norm = max|f(u_star)| (resid_out), retcode and the
+ * Stats counters nsteps/nf/njac/nlinsolve (core.py:68-91).  Counter
+ * pointers may be NULL.  Asynchronous on `stream`. */
+NLK_API int nlk_solve_batch(int32_t handle, int32_t alg, int32_t dtype, int64_t B,
+                    const void* u0_soa, const void* p_soa, double abstol, int32_t maxiters,
+                    void* u_out, void* resid_out, int8_t* retcode_out, int32_t* nsteps_out,
+                    int32_t* nf_out, int32_t* njac_out, int32_t* nlinsolve_out, void* stream);
+
+/* Same contract with HOST buffers (pageable or pinned): the library stages
+ * the batch through device memory in chunks, overlapping host<->device copies
+ * with the solve on `num_streams` streams, and returns when results are in
+ * the host buffers.  This is the call a CPU caller of nlkit switches to. */
+NLK_API int nlk_solve_batch_host(int32_t handle, int32_t alg, int32_t dtype, int64_t B,
+                         const void* u0_soa, const void* p_soa, double abstol, int32_t maxiters,
+                         void* u_out, void* resid_out, int8_t* retcode_out, int32_t* nsteps_out,
+                         int32_t* nf_out, int32_t* njac_out, int32_t* nlinsolve_out,
+                         int64_t chunk, int32_t num_streams);
+
+/* Number of blocks the last nlk_solve_batch launch on this thread used
+ * (diagnostics for the persistent grid). */
+NLK_API int nlk_last_grid(void);
+
+/* Measured FP64 FMA-pipe throughput of the current device in TFLOP/s (8
+ * independent DFMA chains per thread, all SMs; synchronous on `stream`).
+ * The roofline denominator for the solve kernels, which are FP64-issue
+ * bound rather than HBM- or tensor-bound. */
+NLK_API int nlk_fp64_peak(int64_t iters, double* tflops_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NLK_B200_H */

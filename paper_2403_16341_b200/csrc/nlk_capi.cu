@@ -1,0 +1,283 @@
+// C-ABI entry points (include/nlk_b200.h): validation, registry lookup,
+// launch of the persistent solve kernel, and the host-buffer pipeline.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "nlk_b200.h"
+#include "nlk_registry.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_grid = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(NLK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Registry {
+  std::vector<const nlk::Entry*> all;
+  Registry() {
+    const nlk::EntryTable tables[] = {nlk::registry_suite_a(), nlk::registry_suite_b(),
+                                      nlk::registry_suite_c(), nlk::registry_families_a(),
+                                      nlk::registry_families_b(), nlk::registry_families_c(),
+                                      nlk::registry_families_d(), nlk::registry_families_e()};
+    for (const auto& t : tables)
+      for (int i = 0; i < t.count; ++i) all.push_back(&t.entries[i]);
+  }
+};
+const Registry& reg() {
+  static Registry r;
+  return r;
+}
+
+const char* kAlgNames[nlk::NUM_ALGS] = {"newton-raphson", "trust-region", "broyden",
+                                        "klement", "dfsane", "newton-backtracking"};
+
+int validate(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const void* u0, const void* p,
+             double abstol, int32_t maxiters, const void* u_out, const void* resid_out,
+             const void* retcode_out, nlk::Launcher* launcher, const nlk::Entry** entry) {
+  const auto& r = reg();
+  if (handle < 0 || handle >= static_cast<int32_t>(r.all.size()))
+    return fail(NLK_ERR_UNKNOWN_PROBLEM, "invalid problem handle " + std::to_string(handle));
+  if (alg < 0 || alg >= nlk::NUM_ALGS)
+    return fail(NLK_ERR_UNKNOWN_ALG, "invalid algorithm id " + std::to_string(alg));
+  if (dtype != NLK_F64 && dtype != NLK_F32)
+    return fail(NLK_ERR_BAD_ARGUMENT, "dtype must be 0 (f64) or 1 (f32)");
+  if (!(abstol > 0)) return fail(NLK_ERR_BAD_OPTIONS, "abstol must be > 0");
+  if (maxiters < 1) return fail(NLK_ERR_BAD_OPTIONS, "maxiters must be >= 1");
+  if (B < 0) return fail(NLK_ERR_BAD_ARGUMENT, "batch size must be >= 0");
+  const nlk::Entry* e = r.all[handle];
+  if (B > 0) {
+    if (!u0 || !u_out || !resid_out || !retcode_out)
+      return fail(NLK_ERR_BAD_ARGUMENT, "u0, u_out, resid_out and retcode_out are required");
+    if (e->m > 0 && !p)
+      return fail(NLK_ERR_BAD_ARGUMENT, std::string(e->id) + " needs a parameter batch p");
+  }
+  nlk::Launcher l = e->launch[alg][dtype];
+  if (!l)
+    return fail(NLK_ERR_NOT_COMPILED, std::string(e->id) + " n=" + std::to_string(e->n) + " " +
+                                          kAlgNames[alg] + (dtype ? " f32" : " f64") +
+                                          " has no compiled kernel");
+  *launcher = l;
+  *entry = e;
+  return NLK_OK;
+}
+
+int launch(nlk::Launcher l, const nlk::KernelArgs& a0, cudaStream_t s) {
+  nlk::KernelArgs a = a0;
+  unsigned long long* counter = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(*counter), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(counter)");
+  e = cudaMemsetAsync(counter, 0, sizeof(*counter), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
+  a.counter = counter;
+  int grid = 0;
+  e = l(a, s, &grid);
+  g_grid = grid;
+  if (e != cudaSuccess) {
+    cudaFreeAsync(counter, s);
+    return cuda_fail(e, "solve kernel launch");
+  }
+  e = cudaFreeAsync(counter, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(counter)");
+  return NLK_OK;
+}
+
+// Per-device staging workspace for the host-buffer path: device memory and
+// streams are created on first use and grown, never freed per call (a
+// cudaMalloc per call would dominate small batches).  Calls on one device
+// are serialised by the mutex; they are synchronous anyway.
+struct Workspace {
+  std::mutex mu;
+  char* buf = nullptr;
+  size_t cap = 0;
+  std::vector<cudaStream_t> streams;
+};
+Workspace& workspace(int dev) {
+  static Workspace ws[64];
+  return ws[dev & 63];
+}
+
+}  // namespace
+
+extern "C" {
+
+int nlk_version(void) { return 100; }
+
+const char* nlk_last_error(void) { return g_err.c_str(); }
+
+int nlk_last_grid(void) { return g_grid; }
+
+int nlk_alg_lookup(const char* name) {
+  if (!name) return fail(NLK_ERR_UNKNOWN_ALG, "null algorithm name");
+  for (int i = 0; i < nlk::NUM_ALGS; ++i)
+    if (std::strcmp(name, kAlgNames[i]) == 0) return i;
+  return fail(NLK_ERR_UNKNOWN_ALG, std::string("unknown algorithm '") + name + "'");
+}
+
+int nlk_num_problems(void) { return static_cast<int>(reg().all.size()); }
+
+int nlk_problem_info(int32_t handle, const char** id, int32_t* n, int32_t* m) {
+  const auto& r = reg();
+  if (handle < 0 || handle >= static_cast<int32_t>(r.all.size()))
+    return fail(NLK_ERR_UNKNOWN_PROBLEM, "invalid problem handle");
+  if (id) *id = r.all[handle]->id;
+  if (n) *n = r.all[handle]->n;
+  if (m) *m = r.all[handle]->m;
+  return NLK_OK;
+}
+
+int nlk_problem_lookup(const char* id, int32_t n, int32_t* handle, int32_t* n_out, int32_t* m_out) {
+  if (!id) return fail(NLK_ERR_UNKNOWN_PROBLEM, "null problem id");
+  const auto& r = reg();
+  bool known = false;
+  for (size_t h = 0; h < r.all.size(); ++h) {
+    const nlk::Entry* e = r.all[h];
+    if (std::strcmp(e->id, id) != 0) continue;
+    known = true;
+    if (n > 0 && e->n != n) continue;
+    if (handle) *handle = static_cast<int32_t>(h);
+    if (n_out) *n_out = e->n;
+    if (m_out) *m_out = e->m;
+    return NLK_OK;
+  }
+  if (known)
+    return fail(NLK_ERR_BAD_SIZE, std::string(id) + " is not compiled for n=" + std::to_string(n));
+  return fail(NLK_ERR_UNKNOWN_PROBLEM, std::string("unknown problem id '") + id + "'");
+}
+
+int nlk_solve_batch(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const void* u0_soa,
+                    const void* p_soa, double abstol, int32_t maxiters, void* u_out, void* resid_out,
+                    int8_t* retcode_out, int32_t* nsteps_out, int32_t* nf_out, int32_t* njac_out,
+                    int32_t* nlinsolve_out, void* stream) {
+  nlk::Launcher l = nullptr;
+  const nlk::Entry* e = nullptr;
+  int rc = validate(handle, alg, dtype, B, u0_soa, p_soa, abstol, maxiters, u_out, resid_out,
+                    retcode_out, &l, &e);
+  if (rc != NLK_OK) return rc;
+  if (B == 0) return NLK_OK;
+  nlk::KernelArgs a{};
+  a.B = B;
+  a.u0 = u0_soa;
+  a.p = p_soa;
+  a.abstol = abstol;
+  a.maxiters = maxiters;
+  a.u_out = u_out;
+  a.resid_out = resid_out;
+  a.retcode = retcode_out;
+  a.nsteps = nsteps_out;
+  a.nf = nf_out;
+  a.njac = njac_out;
+  a.nlinsolve = nlinsolve_out;
+  return launch(l, a, static_cast<cudaStream_t>(stream));
+}
+
+int nlk_solve_batch_host(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const void* u0_soa,
+                         const void* p_soa, double abstol, int32_t maxiters, void* u_out,
+                         void* resid_out, int8_t* retcode_out, int32_t* nsteps_out, int32_t* nf_out,
+                         int32_t* njac_out, int32_t* nlinsolve_out, int64_t chunk,
+                         int32_t num_streams) {
+  nlk::Launcher l = nullptr;
+  const nlk::Entry* e = nullptr;
+  int rc = validate(handle, alg, dtype, B, u0_soa, p_soa, abstol, maxiters, u_out, resid_out,
+                    retcode_out, &l, &e);
+  if (rc != NLK_OK) return rc;
+  if (B == 0) return NLK_OK;
+  if (chunk <= 0) chunk = std::max<int64_t>(1 << 16, (B + 3) / 4);
+  chunk = std::min<int64_t>(chunk, B);
+  if (num_streams <= 0) num_streams = 3;
+  const int64_t nchunks = (B + chunk - 1) / chunk;
+  num_streams = static_cast<int32_t>(std::min<int64_t>(num_streams, nchunks));
+  const size_t es = dtype == NLK_F64 ? 8 : 4;
+  const int n = e->n, m = e->m;
+  // one device slot per stream: u0 | p | u_out | resid | counters | retcode
+  const size_t slot_bytes = (chunk * es * (2 * n + m + 1) + chunk * 4 * 4 + chunk + 511) & ~size_t(255);
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaGetDevice");
+  Workspace& ws = workspace(dev);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  const size_t need = slot_bytes * num_streams;
+  if (ws.cap < need) {
+    if (ws.buf) cudaFree(ws.buf);
+    ws.buf = nullptr;
+    ws.cap = 0;
+    ce = cudaMalloc(&ws.buf, need);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMalloc(workspace)");
+    ws.cap = need;
+  }
+  while (static_cast<int>(ws.streams.size()) < num_streams) {
+    cudaStream_t st;
+    ce = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamCreate");
+    ws.streams.push_back(st);
+  }
+  std::vector<cudaStream_t> streams(ws.streams.begin(), ws.streams.begin() + num_streams);
+  std::vector<char*> slots(num_streams);
+  for (int s = 0; s < num_streams; ++s) slots[s] = ws.buf + s * slot_bytes;
+  const char* hu0 = static_cast<const char*>(u0_soa);
+  const char* hp = static_cast<const char*>(p_soa);
+  char* huo = static_cast<char*>(u_out);
+  char* hro = static_cast<char*>(resid_out);
+  for (int64_t c = 0; c < nchunks && ce == cudaSuccess && rc == NLK_OK; ++c) {
+    const int s = static_cast<int>(c % num_streams);
+    cudaStream_t st = streams[s];
+    const int64_t lo = c * chunk, len = std::min(chunk, B - lo);
+    char* base = slots[s];
+    char* du0 = base;
+    char* dp = du0 + chunk * es * n;
+    char* duo = dp + chunk * es * m;
+    char* dro = duo + chunk * es * n;
+    int32_t* dcnt = reinterpret_cast<int32_t*>(dro + chunk * es);
+    int8_t* drc = reinterpret_cast<int8_t*>(dcnt + 4 * chunk);
+    // H2D: n (m) strided rows of the SoA host batch into a dense [n][len] block
+    ce = cudaMemcpy2DAsync(du0, len * es, hu0 + lo * es, B * es, len * es, n,
+                           cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess && m > 0)
+      ce = cudaMemcpy2DAsync(dp, len * es, hp + lo * es, B * es, len * es, m,
+                             cudaMemcpyHostToDevice, st);
+    if (ce != cudaSuccess) break;
+    nlk::KernelArgs a{};
+    a.B = len;
+    a.u0 = du0;
+    a.p = m > 0 ? dp : nullptr;
+    a.abstol = abstol;
+    a.maxiters = maxiters;
+    a.u_out = duo;
+    a.resid_out = dro;
+    a.retcode = drc;
+    a.nsteps = nsteps_out ? dcnt : nullptr;
+    a.nf = nf_out ? dcnt + chunk : nullptr;
+    a.njac = njac_out ? dcnt + 2 * chunk : nullptr;
+    a.nlinsolve = nlinsolve_out ? dcnt + 3 * chunk : nullptr;
+    rc = launch(l, a, st);
+    if (rc != NLK_OK) break;
+    ce = cudaMemcpy2DAsync(huo + lo * es, B * es, duo, len * es, len * es, n,
+                           cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(hro + lo * es, dro, len * es, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(retcode_out + lo, drc, len, cudaMemcpyDeviceToHost, st);
+    int32_t* outs[4] = {nsteps_out, nf_out, njac_out, nlinsolve_out};
+    for (int k = 0; k < 4 && ce == cudaSuccess; ++k)
+      if (outs[k]) ce = cudaMemcpyAsync(outs[k] + lo, dcnt + k * chunk, len * 4, cudaMemcpyDeviceToHost, st);
+  }
+  for (int s = 0; s < num_streams; ++s) {
+    cudaError_t e2 = cudaStreamSynchronize(streams[s]);
+    if (ce == cudaSuccess) ce = e2;
+  }
+  if (rc != NLK_OK) return rc;
+  if (ce != cudaSuccess) return cuda_fail(ce, "nlk_solve_batch_host");
+  return NLK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,194 @@
+// Forward-mode dual numbers on the device.
+//
+// Operation-for-operation the arithmetic of nlkit's Dual
+// (/root/reference/pkg/src/nlkit/autodiff.py:45-233) so the device Jacobian is
+// bit-identical to the reference's (the library is compiled with
+// -fmad=false: nothing is contracted unless written as fma()).  W is the seed
+// width of one sweep; the kernels use W = n (one sweep per Jacobian) — every
+// Dual op is componentwise in the partials, so any width gives the same bits
+// as the reference's SEED_WIDTH = 8 chunks (SURVEY.md §7 "Register pressure").
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+namespace nlk {
+
+template <class T> struct Num;  // numeric constants per precision
+template <> struct Num<double> {
+  static constexpr double eps = 2.220446049250313e-16;   // np.finfo(float).eps
+  static constexpr double tiny = 1e-300;                 // solvers.py:22, descent.py:231
+  static constexpr double radius_floor = 1e-308;         // globalize.py:153
+  static constexpr double radius_stop = 1e-300;          // globalize.py:212
+  static constexpr double dbl_min = 2.2250738585072014e-308;
+};
+template <> struct Num<float> {
+  static constexpr float eps = 1.1920929e-07f;
+  static constexpr float tiny = 1e-37f;
+  static constexpr float radius_floor = 1e-37f;
+  static constexpr float radius_stop = 1e-36f;
+  static constexpr float dbl_min = 1.17549435e-38f;
+};
+
+template <int W, class T>
+struct Dual {
+  T v;
+  T d[W];
+};
+
+template <class S> struct ScalarOf { using type = S; };
+template <int W, class T> struct ScalarOf<Dual<W, T>> { using type = T; };
+
+// ---- elementary functions of the float path ---------------------------------
+__device__ __forceinline__ double t_exp(double x) { return exp(x); }
+__device__ __forceinline__ float t_exp(float x) { return expf(x); }
+__device__ __forceinline__ double t_sin(double x) { return sin(x); }
+__device__ __forceinline__ float t_sin(float x) { return sinf(x); }
+__device__ __forceinline__ double t_cos(double x) { return cos(x); }
+__device__ __forceinline__ float t_cos(float x) { return cosf(x); }
+__device__ __forceinline__ double t_atan(double x) { return atan(x); }
+__device__ __forceinline__ float t_atan(float x) { return atanf(x); }
+__device__ __forceinline__ double t_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float t_sqrt(float x) { return sqrtf(x); }
+// Python `x ** 2` / `x ** 3` call glibc pow.  x*x is the correctly rounded
+// square; the cube is formed in double-double and rounded once, which is
+// the correctly rounded cube except in rare near-halfway cases.
+__device__ __forceinline__ double t_pow2(double x) { return x * x; }
+__device__ __forceinline__ float t_pow2(float x) { return x * x; }
+__device__ __forceinline__ double t_pow3(double x) {
+  double hi = x * x;
+  double lo = fma(x, x, -hi);
+  double p = hi * x;
+  double e = fma(hi, x, -p);
+  return p + (e + lo * x);
+}
+__device__ __forceinline__ float t_pow3(float x) { return x * x * x; }
+
+// ---- Dual arithmetic (autodiff.py:66-154) ----------------------------------
+#define NLK_D template <int W, class T> __device__ __forceinline__
+
+NLK_D Dual<W, T> operator+(const Dual<W, T>& a, const Dual<W, T>& b) {
+  Dual<W, T> r; r.v = a.v + b.v;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = a.d[i] + b.d[i];
+  return r;
+}
+NLK_D Dual<W, T> operator+(const Dual<W, T>& a, T c) { Dual<W, T> r = a; r.v = a.v + c; return r; }
+NLK_D Dual<W, T> operator+(T c, const Dual<W, T>& a) { Dual<W, T> r = a; r.v = a.v + c; return r; }
+NLK_D Dual<W, T> operator-(const Dual<W, T>& a, const Dual<W, T>& b) {
+  Dual<W, T> r; r.v = a.v - b.v;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = a.d[i] - b.d[i];
+  return r;
+}
+NLK_D Dual<W, T> operator-(const Dual<W, T>& a, T c) { Dual<W, T> r = a; r.v = a.v - c; return r; }
+NLK_D Dual<W, T> operator-(T c, const Dual<W, T>& a) {  // __rsub__
+  Dual<W, T> r; r.v = c - a.v;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = -a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> operator-(const Dual<W, T>& a) {
+  Dual<W, T> r; r.v = -a.v;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = -a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> operator*(const Dual<W, T>& a, const Dual<W, T>& b) {  // self.v*b + other.v*a
+  Dual<W, T> r; r.v = a.v * b.v;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = a.v * b.d[i] + b.v * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> operator*(const Dual<W, T>& a, T c) {
+  Dual<W, T> r; r.v = a.v * c;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> operator*(T c, const Dual<W, T>& a) { return a * c; }
+NLK_D Dual<W, T> operator/(const Dual<W, T>& a, const Dual<W, T>& b) {  // reciprocal form
+  T inv = T(1) / b.v;
+  T q = a.v * inv;
+  Dual<W, T> r; r.v = q;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = (a.d[i] - q * b.d[i]) * inv;
+  return r;
+}
+NLK_D Dual<W, T> operator/(const Dual<W, T>& a, T c) {
+  T inv = T(1) / c;
+  Dual<W, T> r; r.v = a.v * inv;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = a.d[i] * inv;
+  return r;
+}
+NLK_D Dual<W, T> operator/(T c, const Dual<W, T>& a) {  // __rtruediv__
+  T inv = T(1) / a.v;
+  T q = c * inv;
+  Dual<W, T> r; r.v = q;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = -q * inv * a.d[i];
+  return r;
+}
+NLK_D bool operator>(const Dual<W, T>& a, T c) { return a.v > c; }
+NLK_D bool operator<(const Dual<W, T>& a, T c) { return a.v < c; }
+NLK_D bool operator>=(const Dual<W, T>& a, T c) { return a.v >= c; }
+NLK_D bool operator!=(const Dual<W, T>& a, T c) { return a.v != c; }
+
+// __pow__ n == 2 / n == 3 (autodiff.py:132-136)
+NLK_D Dual<W, T> t_pow2(const Dual<W, T>& a) {
+  Dual<W, T> r; r.v = a.v * a.v;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = T(2) * a.v * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> t_pow3(const Dual<W, T>& a) {
+  T c = T(3) * t_pow2(a.v);
+  Dual<W, T> r; r.v = t_pow3(a.v);
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
+  return r;
+}
+// elementary functions (autodiff.py:189-217)
+NLK_D Dual<W, T> t_exp(const Dual<W, T>& a) {
+  T e = t_exp(a.v);
+  Dual<W, T> r; r.v = e;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = e * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> t_sqrt(const Dual<W, T>& a) {
+  T s = t_sqrt(a.v);
+  T c = T(0.5) / s;
+  Dual<W, T> r; r.v = s;
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> t_sin(const Dual<W, T>& a) {
+  T c = t_cos(a.v);
+  Dual<W, T> r; r.v = t_sin(a.v);
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> t_cos(const Dual<W, T>& a) {
+  T s = t_sin(a.v);
+  Dual<W, T> r; r.v = t_cos(a.v);
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = -s * a.d[i];
+  return r;
+}
+NLK_D Dual<W, T> t_atan(const Dual<W, T>& a) {
+  T c = T(1) / (T(1) + a.v * a.v);
+  Dual<W, T> r; r.v = t_atan(a.v);
+#pragma unroll
+  for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
+  return r;
+}
+#undef NLK_D
+
+__device__ __forceinline__ double value_of(double x) { return x; }
+__device__ __forceinline__ float value_of(float x) { return x; }
+template <int W, class T> __device__ __forceinline__ T value_of(const Dual<W, T>& x) { return x.v; }
+
+}  // namespace nlk

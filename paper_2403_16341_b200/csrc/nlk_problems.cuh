@@ -1,0 +1,420 @@
+// Device residual registry: the built-in problems of nlkit's problem library
+// (/root/reference/pkg/src/nlkit/problems.py), compiled into the solve kernels.
+//
+// Each residual is a template over the scalar type S:
+//   S = T (double / float)  -> the float path (numpy float64 evaluation,
+//                              CountedResidual.at, core.py:119-123)
+//   S = Dual<W, T>          -> the dual path (object arrays of Dual,
+//                              autodiff.forward_sweep, autodiff.py:286-309)
+// Expression trees follow the Python source literally (left-associative,
+// no contraction) so the float path and the Jacobian are bit-identical to the
+// reference wherever only + - * / sqrt are involved.  Where numpy evaluates the
+// two paths differently (pairwise vs sequential sums, BLAS vs object matmul),
+// the helpers below branch on the path.
+#pragma once
+#include "nlk_blas.cuh"
+
+namespace nlk {
+
+template <class S> struct IsDual { static constexpr bool value = false; };
+template <int W, class T> struct IsDual<Dual<W, T>> { static constexpr bool value = true; };
+
+#define NLK_FD __device__ __forceinline__
+#define K(x) (static_cast<T>(x))
+
+template <class S> NLK_FD S zero_of(const S& like) {
+  S r = like;
+  if constexpr (IsDual<S>::value) {
+    r.v = 0;
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(r.d) / sizeof(r.d[0])); ++i) r.d[i] = 0;
+  } else {
+    r = S(0);
+  }
+  return r;
+}
+
+// numpy add.reduce: float64 arrays pairwise (8 accumulators for n >= 8,
+// sequential from 0.0 below); object arrays strictly left to right.
+template <int N, class S> NLK_FD S np_sum(const S* x) {
+  using T = typename ScalarOf<S>::type;
+  if constexpr (IsDual<S>::value) {
+    S r = x[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) r = r + x[i];
+    return r;
+  } else if constexpr (N < 8) {
+    S r = K(0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) r = r + x[i];
+    return r;
+  } else {
+    S r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = x[j];
+    constexpr int NB = N - (N % 8);
+#pragma unroll
+    for (int i = 8; i < NB; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = r[j] + x[i + j];
+    S res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+    for (int i = NB; i < N; ++i) res = res + x[i];
+    return res;
+  }
+}
+template <int N, class S> NLK_FD S np_prod(const S* x) {
+  using T = typename ScalarOf<S>::type;
+  if constexpr (IsDual<S>::value) {
+    S r = x[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) r = r * x[i];
+    return r;
+  } else {
+    S r = K(1);
+#pragma unroll
+    for (int i = 0; i < N; ++i) r = r * x[i];
+    return r;
+  }
+}
+
+// ---- the 23-member suite (problems.py:36-292) -------------------------------
+struct Rosenbrock {  // 36-40
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = K(1.0) - x[0];
+    out[1] = K(10.0) * (x[1] - x[0] * x[0]);
+  }
+};
+struct PowellSingular {  // 43-49
+  static constexpr int N = 4, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = x[0] + K(10.0) * x[1];
+    out[1] = K(2.23606797749979) * (x[2] - x[3]);     // math.sqrt(5.0)
+    out[2] = t_pow2(x[1] - K(2.0) * x[2]);
+    out[3] = K(3.1622776601683795) * t_pow2(x[0] - x[3]);  // math.sqrt(10.0)
+  }
+};
+struct PowellBadlyScaled {  // 52-56
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = K(1e4) * x[0] * x[1] - K(1.0);
+    out[1] = t_exp(-x[0]) + t_exp(-x[1]) - K(1.0001);
+  }
+};
+struct Wood {  // 59-67
+  static constexpr int N = 4, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = K(-200.0) * x[0] * (x[1] - t_pow2(x[0])) - (K(1.0) - x[0]);
+    out[1] = (K(200.0) * (x[1] - t_pow2(x[0])) + K(20.2) * (x[1] - K(1.0)) + K(19.8) * (x[3] - K(1.0)));
+    out[2] = K(-180.0) * x[2] * (x[3] - t_pow2(x[2])) - (K(1.0) - x[2]);
+    out[3] = (K(180.0) * (x[3] - t_pow2(x[2])) + K(20.2) * (x[3] - K(1.0)) + K(19.8) * (x[1] - K(1.0)));
+  }
+};
+struct HelicalValley {  // 70-81
+  static constexpr int N = 3, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    const T twopi = K(6.283185307179586);  // 2.0 * math.pi
+    if (x[0] > K(0)) {
+      S angle = t_atan(x[1] / x[0]) / twopi;
+      out[0] = K(10.0) * (x[2] - K(10.0) * angle);
+    } else if (x[0] < K(0)) {
+      S angle = t_atan(x[1] / x[0]) / twopi + K(0.5);
+      out[0] = K(10.0) * (x[2] - K(10.0) * angle);
+    } else {
+      T angle = (x[1] >= K(0)) ? K(0.25) : K(-0.25);
+      out[0] = K(10.0) * (x[2] - K(10.0) * angle);
+    }
+    out[1] = K(10.0) * (t_sqrt(x[0] * x[0] + x[1] * x[1]) - K(1.0));
+    out[2] = x[2];
+  }
+};
+struct Watson {  // 84-109 (n = 2)
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+#pragma unroll 1
+    for (int i = 1; i < 30; ++i) {
+      T ti = T(i) / K(29.0);
+      // sum1 over j = 1 .. n-1 from the float 0.0
+      T temp = K(1.0);
+      S sum1 = K(0.0) + (K(1.0) * temp) * x[1];
+      temp = temp * ti;
+      S sum2 = K(0.0) + K(1.0) * x[0];
+      temp = K(1.0) * ti;
+      sum2 = sum2 + temp * x[1];
+      S temp1 = sum1 - sum2 * sum2 - K(1.0);
+      S temp2 = K(2.0) * ti * sum2;
+      T tk = K(1.0) / ti;
+      S t0 = tk * (K(0.0) - temp2) * temp1;
+      tk = tk * ti;
+      S t1 = tk * (K(1.0) - temp2) * temp1;
+      if (i == 1) {
+        out[0] = K(0.0) + t0;
+        out[1] = K(0.0) + t1;
+      } else {
+        out[0] = out[0] + t0;
+        out[1] = out[1] + t1;
+      }
+    }
+    S t = x[1] - x[0] * x[0] - K(1.0);
+    out[0] = out[0] + x[0] * (K(1.0) - K(2.0) * t);
+    out[1] = out[1] + t;
+  }
+};
+struct Chebyquad {  // 112-129 (n = 2)
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      S t_cur = K(2.0) * x[j] - K(1.0);
+      S scale = K(2.0) * t_cur;
+      S t_prev = t_cur;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        out[i] = (j == 0) ? K(0.0) + t_cur : out[i] + t_cur;
+        S t_next = (i == 0) ? scale * t_cur - K(1.0) : scale * t_cur - t_prev;
+        t_prev = t_cur;
+        t_cur = t_next;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      out[k] = out[k] / T(N);
+      if ((k + 1) % 2 == 0) out[k] = out[k] + K(1.0) / (T((k + 1) * (k + 1)) - K(1.0));
+    }
+  }
+};
+struct BrownAlmostLinear {  // 132-139
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    S total = np_sum<N>(x);
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) out[k] = x[k] + total - K(N + 1.0);
+    out[N - 1] = np_prod<N>(x) - K(1.0);
+  }
+};
+struct DiscreteBoundaryValue {  // 142-151
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    const T h = K(1.0) / T(N + 1);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      T tk = T(k + 1) * h;
+      S a = K(2.0) * x[k];
+      a = (k > 0) ? a - x[k > 0 ? k - 1 : 0] : a - K(0.0);
+      a = (k < N - 1) ? a - x[k < N - 1 ? k + 1 : 0] : a - K(0.0);
+      out[k] = a + K(0.5) * h * h * t_pow3(x[k] + tk + K(1.0));
+    }
+  }
+};
+struct DiscreteIntegral {  // 154-168
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    const T h = K(1.0) / T(N + 1);
+    T t[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) t[j] = T(j + 1) * h;
+    S cubes[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) cubes[j] = t_pow3(x[j] + t[j] + K(1.0));
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      S s1 = K(0.0) + t[0] * cubes[0];
+#pragma unroll
+      for (int j = 1; j <= k; ++j) s1 = s1 + t[j] * cubes[j];
+      S inner = (K(1.0) - t[k]) * s1;
+      if (k + 1 < N) {
+        S s2 = K(0.0) + (K(1.0) - t[k + 1 < N ? k + 1 : 0]) * cubes[k + 1 < N ? k + 1 : 0];
+#pragma unroll
+        for (int j = k + 2; j < N; ++j) s2 = s2 + (K(1.0) - t[j]) * cubes[j];
+        inner = inner + t[k] * s2;
+      } else {
+        inner = inner + t[k] * K(0.0);
+      }
+      out[k] = x[k] + K(0.5) * h * inner;
+    }
+  }
+};
+struct Trigonometric {  // 171-177
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    S c[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) c[k] = t_cos(x[k]);
+    S cos_sum = np_sum<N>(c);
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      out[k] = T(N) - cos_sum + T(k + 1) * (K(1.0) - t_cos(x[k])) - t_sin(x[k]);
+  }
+};
+struct VariablyDimensioned {  // 180-188
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    S w[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) w[k] = T(k + 1) * (x[k] - K(1.0));
+    S s = np_sum<N>(w);
+    S temp = s * (K(1.0) + K(2.0) * s * s);
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = x[k] - K(1.0) + T(k + 1) * temp;
+  }
+};
+template <int NN>
+struct BroydenTridiagonal {  // 191-198 (n-generic)
+  static constexpr int N = NN, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      S a = (K(3.0) - K(2.0) * x[k]) * x[k];
+      a = (k > 0) ? a - x[k > 0 ? k - 1 : 0] : a - K(0.0);
+      a = (k < N - 1) ? a - K(2.0) * x[k < N - 1 ? k + 1 : 0] : a - K(2.0) * K(0.0);
+      out[k] = a + K(1.0);
+    }
+  }
+};
+struct BroydenBanded {  // 201-210
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int lo = k - 5 > 0 ? k - 5 : 0;
+      const int hi = k + 2 < N ? k + 2 : N;
+      S acc = x[0];
+      bool first = true;
+#pragma unroll
+      for (int j = lo; j < hi; ++j) {
+        if (j == k) continue;
+        S term = x[j] * (K(1.0) + x[j]);
+        acc = first ? K(0.0) + term : acc + term;
+        first = false;
+      }
+      out[k] = x[k] * (K(2.0) + K(5.0) * x[k] * x[k]) + K(1.0) - acc;
+    }
+  }
+};
+struct MatrixSqrt2x2 {  // 213-220
+  static constexpr int N = 4, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = x[0] * x[0] + x[1] * x[2] - K(1e-4);
+    out[1] = x[0] * x[1] + x[1] * x[3] - K(1.0);
+    out[2] = x[2] * x[0] + x[3] * x[2];
+    out[3] = x[2] * x[1] + x[3] * x[3] - K(1e-4);
+  }
+};
+struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
+  static constexpr int N = 9, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        S r;
+        if constexpr (IsDual<S>::value) {  // object matmul: first product, then adds
+          r = x[i * 3 + 0] * x[0 * 3 + j];
+          r = r + x[i * 3 + 1] * x[1 * 3 + j];
+          r = r + x[i * 3 + 2] * x[2 * 3 + j];
+        } else {  // dgemm: FMA chain from a plain product
+          r = x[i * 3 + 0] * x[0 * 3 + j];
+          r = t_fma(x[i * 3 + 1], x[1 * 3 + j], r);
+          r = t_fma(x[i * 3 + 2], x[2 * 3 + j], r);
+        }
+        const int k = i * 3 + j;
+        const T a = (k == 0 || k == 4 || k == 8) ? K(1e-4) : (k == 1 ? K(1.0) : K(0.0));
+        out[k] = r - a;
+      }
+  }
+};
+struct DennisSchnabel {  // 233-237
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = x[0] * x[0] + x[1] * x[1] - K(2.0);
+    out[1] = t_exp(x[0] - K(1.0)) + t_pow3(x[1]) - K(2.0);
+  }
+};
+struct ProductExponential {  // 240-251
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    if (x[0] != K(0)) out[0] = x[1] * x[1] * (K(1.0) - t_exp(-x[0] * x[0])) / x[0];
+    else out[0] = K(0.0) * x[1];
+    if (x[1] != K(0)) out[1] = x[0] * (K(1.0) - t_exp(-x[1] * x[1])) / x[1];
+    else out[1] = K(0.0) * x[0];
+  }
+};
+struct CubicRadial {  // 254-260
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    S r2 = x[0] * x[0] + x[1] * x[1];
+    out[0] = x[0] * r2;
+    out[1] = x[1] * r2;
+  }
+};
+struct DoubleRootScalar {  // 263-266
+  static constexpr int N = 1, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = x[0] * t_pow2(x[0] - K(5.0));
+  }
+};
+struct FreudensteinRoth {  // 269-273
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = K(-13.0) + x[0] + ((K(5.0) - x[1]) * x[1] - K(2.0)) * x[1];
+    out[1] = K(-29.0) + x[0] + ((K(1.0) + x[1]) * x[1] - K(14.0)) * x[1];
+  }
+};
+struct Boggs {  // 276-280
+  static constexpr int N = 2, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = x[0] * x[0] - x[1] + K(1.0);
+    out[1] = x[0] - t_cos(K(1.5707963267948966) * x[1]);  // (0.5 * math.pi) * x1
+  }
+};
+struct Chandrasekhar {  // 286-292
+  static constexpr int N = 10, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    T mu[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) mu[i] = (T(i + 1) - K(0.5)) / T(N);
+    const T c = K(0.9) / (K(2.0) * T(N));
+    S y[N];
+    if constexpr (IsDual<S>::value) {  // object matmul: first product, then adds
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        y[i] = x[0] * (mu[i] / (mu[i] + mu[0]));
+#pragma unroll
+        for (int k = 1; k < N; ++k) y[i] = y[i] + x[k] * (mu[i] / (mu[i] + mu[k]));
+      }
+    } else {  // BLAS dgemv_t on the C-ordered A (column-major copy here)
+      T A[N * N];
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int k = 0; k < N; ++k) A[r + k * N] = mu[r] / (mu[r] + mu[k]);
+      gemv_A_x<N>(A, x, y);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = x[i] - K(1.0) / (K(1.0) - c * y[i]);
+  }
+};
+
+// ---- parametrised families (problems.py:358-387) ----------------------------
+template <int NN>
+struct GeneralizedRosenbrock {  // 363-368
+  static constexpr int N = NN, M = 0;
+  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+    out[0] = K(1.0) - x[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) out[i] = K(10.0) * (x[i] - x[i - 1] * x[i - 1]);
+  }
+};
+template <int NN>
+struct Quadratic {  // 382-383: u * u - theta
+  static constexpr int N = NN, M = NN;
+  template <class S, class T> NLK_FD static void f(const S* x, const T* p, S* out) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];
+  }
+};
+
+#undef K
+#undef NLK_FD
+}  // namespace nlk

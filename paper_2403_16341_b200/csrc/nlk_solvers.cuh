@@ -1,0 +1,486 @@
+// Per-system solver state machines: one outer iteration per step() call.
+//
+// Each solver restates one nlkit driver for a single system held in
+// registers; the persistent kernel (nlk_kernel.cuh) interleaves steps of
+// different systems in the lanes of a warp and refills finished lanes.
+//   NewtonRaphson  solvers.py:179-287   (+ line search: solvers.py:263-276,
+//                                        globalize.py:40-74)
+//   TrustRegion    globalize.py:156-214, descent.py:78-106, globalize.py:116-153
+//   Broyden        solvers.py:290-358, quasinewton.py:66-121,179-193
+//   Klement        solvers.py:290-358, quasinewton.py:152-168,194-198
+//   DFSane         builder-authored (oracle/dfsane_ref.py)
+// Counters follow the reference exactly: nf counts every residual evaluation
+// including ceil(n/8) dual sweeps per Jacobian, njac Jacobians, nlinsolve
+// linear solves (TR: loop iterations; QN: inverse applications), nsteps
+// accepted steps.
+#pragma once
+#include "nlk_problems.cuh"
+
+namespace nlk {
+
+enum RetCode : int { SUCCESS = 0, MAXITERS = 1, LINESEARCH_FAILED = 2, LINSOLVE_FAILED = 3,
+                     STALLED = 4, NONFINITE = 5, RUNNING = -1 };
+enum Alg : int { ALG_NR = 0, ALG_TR = 1, ALG_BROYDEN = 2, ALG_KLEMENT = 3, ALG_DFSANE = 4,
+                 ALG_NEWTON_LS = 5, NUM_ALGS = 6 };
+
+#define NLK_FD __device__ __forceinline__
+
+template <int N, class T> NLK_FD bool all_finite(const T* x) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < N; ++i) ok &= isfinite(x[i]);
+  return ok;
+}
+// np.max(np.abs(x)) with NaN propagation
+template <int N, class T> NLK_FD T max_abs(const T* x) {
+  T m = fabs(x[0]);
+  bool nan = (m != m);
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    T a = fabs(x[i]);
+    nan |= (a != a);
+    m = a > m ? a : m;
+  }
+  return nan ? T(NAN) : m;
+}
+template <int N, class T> NLK_FD bool converged(const T* f, T abstol) {  // core.py:94-98
+  T m = max_abs<N>(f);
+  return isfinite(m) && m <= abstol;
+}
+
+// Width of one dual sweep on the device (register pressure only; bits are
+// independent of it).  The reference sweeps in SEED_WIDTH = 8 chunks.
+template <int N> struct SweepWidth { static constexpr int value = N <= 4 ? N : 4; };
+
+// dense_jacobian (autodiff.py:342-355) into column-major J.  Returns -1 on
+// success, else the index of the reference chunk (8 columns) whose check
+// raised NonFiniteValue — nlkit evaluates chunks up to and including it.
+template <class P, int N, class T, int C0>
+NLK_FD void jac_sweeps(const T* u, const T* p, T* J, bool& vals_ok, int& bad_col) {
+  if constexpr (C0 < N) {
+    constexpr int SW = SweepWidth<N>::value;
+    constexpr int W = (N - C0) < SW ? (N - C0) : SW;
+    Dual<W, T> xd[N], out[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      xd[i].v = u[i];
+#pragma unroll
+      for (int j = 0; j < W; ++j) xd[i].d[j] = (i == C0 + j) ? T(1) : T(0);
+    }
+    P::template f<Dual<W, T>, T>(xd, p, out);
+    if constexpr (C0 == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) vals_ok &= isfinite(out[i].v);
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      bool colok = true;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        colok &= isfinite(out[i].d[j]);
+        J[i + (C0 + j) * N] = out[i].d[j];
+      }
+      if (!colok && bad_col > C0 + j) bad_col = C0 + j;
+    }
+    jac_sweeps<P, N, T, C0 + W>(u, p, J, vals_ok, bad_col);
+  }
+}
+
+template <class P, int N, class T>
+NLK_FD int jacobian(const T* u, const T* p, T* J) {
+  bool vals_ok = true;
+  int bad_col = N;
+  jac_sweeps<P, N, T, 0>(u, p, J, vals_ok, bad_col);
+  if (!vals_ok) return 0;
+  if (bad_col < N) return bad_col / 8;
+  return -1;
+}
+
+template <class P, int N, class T>
+struct Base {
+  static constexpr int M = P::M;
+  T u[N], f[N];
+  T p[M > 0 ? M : 1];
+  int k, nsteps, nf, njac, nlinsolve;
+
+  NLK_FD void F(const T* x, T* out) {  // CountedResidual.at (core.py:119-123)
+    nf += 1;
+    P::template f<T, T>(x, p, out);
+  }
+  NLK_FD int jac(T* J) {
+    njac += 1;
+    int bad = jacobian<P, N, T>(u, p, J);
+    constexpr int chunks = (N + 7) / 8;
+    nf += (bad < 0) ? chunks : bad + 1;
+    return bad;
+  }
+  // shared prologue of every driver: f(u0), NONFINITE / already-converged
+  NLK_FD int start(T abstol) {
+    k = nsteps = nf = njac = nlinsolve = 0;
+    F(u, f);
+    if (!all_finite<N>(f)) return NONFINITE;
+    if (converged<N>(f, abstol)) return SUCCESS;
+    return RUNNING;
+  }
+};
+
+// ---- Newton-Raphson (optionally with backtracking line search) --------------
+template <class P, int N, class T, bool LS>
+struct NewtonRaphson : Base<P, N, T> {
+  using B = Base<P, N, T>;
+  NLK_FD int init(T abstol) { return B::start(abstol); }
+  NLK_FD int step(T abstol, int maxiters) {
+    B::k += 1;
+    T J[N * N];
+    int piv[N];
+    if (B::jac(J) >= 0) return NONFINITE;
+    T Jf[LS ? N * N : 1];
+    if constexpr (LS) {
+#pragma unroll
+      for (int i = 0; i < N * N; ++i) Jf[i] = J[i];
+    }
+    if (!lu_factor<N>(J, piv)) return LINSOLVE_FAILED;
+    B::nlinsolve += 1;
+    T du[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) du[i] = -B::f[i];
+    getrs<N>(J, piv, du);
+    T alpha = T(1);
+    T un[N], fn[N];
+    if constexpr (LS) {
+      // merit_along + backtracking_search (globalize.py:40-74)
+      T phi0 = T(0.5) * ddot<N>(B::f, B::f);
+      T Jdu[N];
+      gemv_A_x<N>(Jf, du, Jdu);
+      T dphi0 = ddot<N>(B::f, Jdu);
+      if (!(dphi0 < T(0))) return LINESEARCH_FAILED;
+      bool ok = false;
+#pragma unroll 1
+      for (int it = 0; it < 31; ++it) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) un[i] = B::u[i] + alpha * du[i];
+        B::F(un, fn);
+        T value = T(0.5) * ddot<N>(fn, fn);
+        if (value <= phi0 + T(1e-4) * alpha * dphi0) { ok = true; break; }
+        alpha *= T(0.5);
+      }
+      if (!ok) return LINESEARCH_FAILED;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) un[i] = B::u[i] + alpha * du[i];
+    B::F(un, fn);
+    if (!(all_finite<N>(un) && all_finite<N>(fn))) return NONFINITE;
+#pragma unroll
+    for (int i = 0; i < N; ++i) { B::u[i] = un[i]; B::f[i] = fn[i]; }
+    B::nsteps += 1;
+    if (converged<N>(B::f, abstol)) return SUCCESS;
+    return B::k >= maxiters ? MAXITERS : RUNNING;
+  }
+};
+
+// ---- trust region with Powell dogleg -----------------------------------------
+template <class P, int N, class T>
+struct TrustRegion : Base<P, N, T> {
+  using B = Base<P, N, T>;
+  T J[N * N], LU[N * N];
+  int piv[N];
+  T radius, radius_max;
+  bool cached;
+
+  NLK_FD int init(T abstol) {
+    int st = B::start(abstol);
+    T mu = max_abs<N>(B::u);
+    radius = (mu > T(1)) ? mu : T(1);  // initial_trust_state: max(1.0, |u0|_inf)
+    radius_max = T(1e3) * radius;
+    cached = false;
+    return st;
+  }
+  // dogleg_direction (descent.py:78-106)
+  NLK_FD void dogleg(T* out) {
+    T newton[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) newton[i] = -B::f[i];
+    getrs<N>(LU, piv, newton);
+    if (norm2<N>(newton) <= radius) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[i] = newton[i];
+      return;
+    }
+    T g[N], Jg[N], cauchy[N];
+    gemv_AT_x<N>(J, B::f, g);
+    gemv_A_x<N>(J, g, Jg);
+    T gg = ddot<N>(g, g);
+    T jj = ddot<N>(Jg, Jg);
+    T t_star = gg / ((Num<T>::tiny > jj) ? Num<T>::tiny : jj);
+#pragma unroll
+    for (int i = 0; i < N; ++i) cauchy[i] = -t_star * g[i];
+    T cnorm = norm2<N>(cauchy);
+    if (cnorm >= radius) {
+      T s = -(radius / sqrt(gg));
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[i] = s * g[i];
+      return;
+    }
+    T d[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = newton[i] - cauchy[i];
+    T a = ddot<N>(d, d);
+    T b = T(2) * ddot<N>(cauchy, d);
+    T c = cnorm * cnorm - radius * radius;
+    T tau = (-b + sqrt(b * b - T(4) * a * c)) / (T(2) * a);
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = cauchy[i] + tau * d[i];
+  }
+  NLK_FD int step(T abstol, int maxiters) {
+    B::k += 1;
+    if (!cached) {
+      if (B::jac(J) >= 0) return NONFINITE;
+#pragma unroll
+      for (int i = 0; i < N * N; ++i) LU[i] = J[i];
+      if (!lu_factor<N>(LU, piv)) return LINSOLVE_FAILED;
+      cached = true;
+    }
+    B::nlinsolve += 1;
+    T du[N];
+    dogleg(du);
+    if (!all_finite<N>(du)) return LINSOLVE_FAILED;
+    T ut[N], ft[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) ut[i] = B::u[i] + du[i];
+    B::F(ut, ft);
+    T rho;
+    if (all_finite<N>(ft)) {  // tr_ratio (globalize.py:121-134)
+      T Jdu[N], model[N];
+      gemv_A_x<N>(J, du, Jdu);
+#pragma unroll
+      for (int i = 0; i < N; ++i) model[i] = B::f[i] + Jdu[i];
+      T ff = ddot<N>(B::f, B::f);
+      T actual = ff - ddot<N>(ft, ft);
+      T predicted = ff - ddot<N>(model, model);
+      rho = (predicted < Num<T>::eps * ff) ? T(-INFINITY) : actual / predicted;
+    } else {
+      rho = T(-INFINITY);
+    }
+    bool accept;  // tr_update, SIMPLE scheme (globalize.py:137-153)
+    if (rho >= T(0.5)) {
+      T ex = T(2) * radius;
+      radius = (radius_max < ex) ? radius_max : ex;
+      accept = true;
+    } else if (rho >= T(0.1)) {
+      accept = true;
+    } else {
+      T sh = T(0.5) * radius;
+      radius = (Num<T>::radius_floor > sh) ? Num<T>::radius_floor : sh;
+      accept = false;
+    }
+    if (accept) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) { B::u[i] = ut[i]; B::f[i] = ft[i]; }
+      B::nsteps += 1;
+      cached = false;
+      if (converged<N>(B::f, abstol)) return SUCCESS;
+    }
+    if (radius < Num<T>::radius_stop) return MAXITERS;
+    return B::k >= maxiters ? MAXITERS : RUNNING;
+  }
+};
+
+// ---- quasi-Newton: dense inverse Broyden / diagonal Klement ------------------
+template <class P, int N, class T, bool DIAG>
+struct QuasiNewton : Base<P, N, T> {
+  using B = Base<P, N, T>;
+  T H[DIAG ? N : N * N];  // inverse Jacobian (column-major) or Jacobian diagonal
+  int reinits, since;
+  // stalling window (Klement): min of hist[:-3] and the last three entries
+  T prev_min, last[3];
+  int hlen;
+
+  NLK_FD void qn_init() {  // IDENTITY_INIT (quasinewton.py:66-94)
+    if constexpr (DIAG) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) H[i] = T(1);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N * N; ++i) H[i] = (i % N == i / N) ? T(1) : T(0);
+    }
+  }
+  NLK_FD void hist_reset(T v) { hlen = 1; last[2] = v; prev_min = T(INFINITY); }
+  NLK_FD void hist_push(T v) {
+    if (hlen >= 3) { T old = last[0]; prev_min = (hlen == 3 || old < prev_min) ? old : prev_min; }
+    last[0] = last[1]; last[1] = last[2]; last[2] = v;
+    hlen += 1;
+  }
+  NLK_FD int init(T abstol) {
+    int st = B::start(abstol);
+    qn_init();
+    reinits = 0;
+    since = 0;
+    if constexpr (DIAG) hist_reset(norm2<N>(B::f));
+    return st;
+  }
+  NLK_FD int step(T abstol, int maxiters) {
+    B::k += 1;
+    T du[N];
+    if constexpr (DIAG) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) du[i] = -(B::f[i] / H[i]);
+    } else {
+      T Hf[N];
+      gemv_A_x<N>(H, B::f, Hf);
+#pragma unroll
+      for (int i = 0; i < N; ++i) du[i] = -Hf[i];
+    }
+    B::nlinsolve += 1;
+    T un[N], fn[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) un[i] = B::u[i] + T(1) * du[i];
+    B::F(un, fn);
+    if (!(all_finite<N>(un) && all_finite<N>(fn))) return NONFINITE;
+    T nnew = norm2<N>(fn);
+    bool merit_decreased = nnew < norm2<N>(B::f);
+    T s[N], t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      s[i] = un[i] - B::u[i];
+      t[i] = fn[i] - B::f[i];
+      B::u[i] = un[i];
+      B::f[i] = fn[i];
+    }
+    B::nsteps += 1;
+    if constexpr (DIAG) hist_push(nnew);
+    if (converged<N>(B::f, abstol)) return SUCCESS;
+    bool reinit;
+    if constexpr (!DIAG) {  // NOT_DESCENT (quasinewton.py:188-193)
+      T mdu = max_abs<N>(du);
+      T mu = max_abs<N>(B::u);
+      T scale = (T(1) > mu) ? T(1) : mu;
+      reinit = !merit_decreased || (mdu < Num<T>::eps * scale);
+    } else {  // STALLING, window 3 (quasinewton.py:194-198)
+      if (hlen < 4) {
+        reinit = false;
+      } else {
+        T recent = last[0];
+        recent = last[1] < recent ? last[1] : recent;
+        recent = last[2] < recent ? last[2] : recent;
+        reinit = recent > prev_min * T(1.0 - 1e-12);
+      }
+    }
+    if (reinit) {
+      if (reinits > 0 && since <= 1) return STALLED;
+      reinits += 1;
+      qn_init();
+      since = 0;
+      if constexpr (DIAG) hist_reset(norm2<N>(B::f));
+    } else {
+      if constexpr (DIAG) {  // klement_update (quasinewton.py:152-168)
+        T thresh = T(1e-9) * max_abs<N>(s);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          if (fabs(s[i]) > thresh) H[i] = t[i] / s[i];
+          if (fabs(H[i]) < T(1e-12)) H[i] = (H[i] >= T(0)) ? T(1e-12) : T(-1e-12);
+        }
+      } else {  // broyden_update (quasinewton.py:107-121)
+        T Ht[N], sH[N];
+        gemv_A_x<N>(H, t, Ht);
+        gemv_AT_x<N>(H, s, sH);
+        T denom = ddot<N>(s, Ht);
+        if (!(fabs(denom) < T(1e-12) * norm2<N>(s) * norm2<N>(Ht))) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            T a = s[i] - Ht[i];
+#pragma unroll
+            for (int j = 0; j < N; ++j) H[i + j * N] = H[i + j * N] + a * sH[j] / denom;
+          }
+        }
+      }
+      since += 1;
+    }
+    return B::k >= maxiters ? MAXITERS : RUNNING;
+  }
+};
+
+// ---- DFSane (builder-authored) ------------------------------
+template <class P, int N, class T>
+struct DFSane : Base<P, N, T> {
+  using B = Base<P, N, T>;
+  static constexpr int MEM = 10;
+  T fnorm, f0, sigma;
+  T hist[MEM];
+
+  NLK_FD int init(T abstol) {
+    int st = B::start(abstol);
+    fnorm = ddot<N>(B::f, B::f);
+    f0 = fnorm;
+#pragma unroll
+    for (int i = 0; i < MEM; ++i) hist[i] = fnorm;
+    sigma = T(1);
+    return st;
+  }
+  NLK_FD int step(T abstol, int maxiters) {
+    B::k += 1;
+    T as = fabs(sigma);
+    T cl = as < T(1e-10) ? T(1e-10) : (as > T(1e10) ? T(1e10) : as);
+    sigma = (sigma >= T(0)) ? cl : -cl;
+    T d[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = -sigma * B::f[i];
+    T eta = f0 / (T(B::k) * T(B::k));
+    T fbar = hist[0];
+#pragma unroll
+    for (int i = 1; i < MEM; ++i) fbar = hist[i] > fbar ? hist[i] : fbar;
+    T ap = T(1), am = T(1);
+    T ua[N], fa[N], na;
+#pragma unroll 1
+    for (int ls = 0;; ++ls) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) ua[i] = B::u[i] + ap * d[i];
+      B::F(ua, fa);
+      T np_ = ddot<N>(fa, fa);
+      if (np_ <= fbar + eta - T(1e-4) * (ap * ap) * fnorm) { na = np_; break; }
+#pragma unroll
+      for (int i = 0; i < N; ++i) ua[i] = B::u[i] - am * d[i];
+      B::F(ua, fa);
+      T nm = ddot<N>(fa, fa);
+      if (nm <= fbar + eta - T(1e-4) * (am * am) * fnorm) { na = nm; break; }
+      if (ls == 100) return LINESEARCH_FAILED;
+      T tp = (ap * ap) * fnorm / (np_ + (T(2) * ap - T(1)) * fnorm);
+      T tm = (am * am) * fnorm / (nm + (T(2) * am - T(1)) * fnorm);
+      T lo = T(0.1) * ap, hi = T(0.5) * ap;
+      ap = !(tp > lo) ? lo : (tp > hi ? hi : tp);
+      lo = T(0.1) * am; hi = T(0.5) * am;
+      am = !(tm > lo) ? lo : (tm > hi ? hi : tm);
+    }
+    if (!(all_finite<N>(ua) && all_finite<N>(fa))) return NONFINITE;
+    T s[N], y[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      s[i] = ua[i] - B::u[i];
+      y[i] = fa[i] - B::f[i];
+      B::u[i] = ua[i];
+      B::f[i] = fa[i];
+    }
+    fnorm = na;
+    B::nsteps += 1;
+    const int slot = B::k % MEM;
+#pragma unroll
+    for (int i = 0; i < MEM; ++i)
+      if (i == slot) hist[i] = fnorm;
+    if (converged<N>(B::f, abstol)) return SUCCESS;
+    T ss = ddot<N>(s, s);
+    T sy = ddot<N>(s, y);
+    sigma = ss / sy;
+    if (sigma != sigma) sigma = T(1);
+    return B::k >= maxiters ? MAXITERS : RUNNING;
+  }
+};
+
+template <class P, int N, class T, int ALG> struct SolverOf;
+template <class P, int N, class T> struct SolverOf<P, N, T, ALG_NR> { using type = NewtonRaphson<P, N, T, false>; };
+template <class P, int N, class T> struct SolverOf<P, N, T, ALG_NEWTON_LS> { using type = NewtonRaphson<P, N, T, true>; };
+template <class P, int N, class T> struct SolverOf<P, N, T, ALG_TR> { using type = TrustRegion<P, N, T>; };
+template <class P, int N, class T> struct SolverOf<P, N, T, ALG_BROYDEN> { using type = QuasiNewton<P, N, T, false>; };
+template <class P, int N, class T> struct SolverOf<P, N, T, ALG_KLEMENT> { using type = QuasiNewton<P, N, T, true>; };
+template <class P, int N, class T> struct SolverOf<P, N, T, ALG_DFSANE> { using type = DFSane<P, N, T>; };
+
+#undef NLK_FD
+}  // namespace nlk

@@ -1,0 +1,174 @@
+"""Parity of the CUDA kernels (through the C-ABI) with the reference.
+
+Three layers, all on identical inputs:
+  1. golden fixtures produced by the unmodified reference (small samples of
+     every BASELINE.json config, all five algorithms + newton-backtracking);
+  2. the oracle restatement at larger samples (20k systems per C2 problem);
+  3. size-independent properties at full size (1M systems): known roots,
+     determinism, permutation invariance, host-buffer path == device path.
+
+Arithmetic classes:
+  EXACT  only + - * / sqrt and BLAS/LAPACK models: every output bit-identical
+         to the reference, counters included — even on roundoff-sensitive
+         systems, because the rounding sequence is the same;
+  POW    Python `x**2`/`x**3` (glibc pow, not correctly rounded in ~0.1% of
+         cases; the device rounds x^2, x^3 correctly): retcode/nsteps exact
+         outside the sensitivity mask, u to 1e-10 relative;
+  TRANS  exp/sin/cos/atan (numpy SIMD exp, glibc vs CUDA libdevice last
+         bits): retcode/nsteps exact outside the mask (<= 2 % slack for
+         last-bit flips the one-ulp mask cannot see), resid <= abstol on
+         success.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import close, golden_case, load_manifest
+from paper_2403_16341_b200 import _lib, solvers, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+POW = {"test23/powell-singular", "test23/wood", "test23/double-root-scalar",
+       "test23/discrete-boundary-value", "test23/discrete-integral"}
+TRANS = {"test23/powell-badly-scaled", "test23/helical-valley", "test23/trigonometric",
+         "test23/dennis-schnabel", "test23/product-exponential", "test23/boggs"}
+
+CASES = load_manifest()["cases"]
+
+
+def klass(pid):
+    return "trans" if pid in TRANS else ("pow" if pid in POW else "exact")
+
+
+def gpu_solve(pid, alg, u0, p=None, abstol=1e-8, maxiters=1000, dtype=torch.float64):
+    r = solvers.solve_batch(pid, u0, p, alg, solvers.SolveOptions(abstol, maxiters),
+                            dtype=dtype, n=u0.shape[1])
+    return r.to_numpy()
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+def check_against(ref, got, pid, mask, what):
+    same = (got["retcode"] == ref["retcode"]) & (got["nsteps"] == ref["nsteps"])
+    k = klass(pid)
+    if k == "exact":
+        assert same.all(), f"{what}: retcode/nsteps differ at {np.nonzero(~same)[0][:10]}"
+        for c in ("nf", "njac", "nlinsolve"):
+            assert np.array_equal(got[c], ref[c]), f"{what}: {c}"
+        assert np.array_equal(bits(got["u"]), bits(ref["u"])), f"{what}: u bits"
+        assert np.array_equal(bits(got["resid"]), bits(ref["resid"])), f"{what}: resid bits"
+        return
+    bad = ~same & ~mask
+    slack = 0 if k == "pow" else max(1, int(0.02 * len(same)))
+    assert bad.sum() <= slack, f"{what}: {bad.sum()} unmasked retcode/nsteps mismatches"
+    succ = same & (ref["retcode"] == 0)
+    assert (got["resid"][succ] <= 1e-8).all()
+    if k == "pow":
+        assert close(got["u"][succ], ref["u"][succ], 1e-10).all(), f"{what}: u tolerance"
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["case"] for c in CASES])
+def test_golden(case):
+    g = golden_case(case)
+    p = g["p"] if g["p"].shape[1] else None
+    got = gpu_solve(case["problem_id"], case["alg"], g["u0"], p)
+    check_against(g, got, case["problem_id"], g["sensitive"], case["case"])
+
+
+@pytest.mark.parametrize("alg", ["newton-raphson", "trust-region"])
+@pytest.mark.parametrize("index", range(1, 24))
+def test_oracle_c2_sample(index, alg):
+    from oracle import oracle as O
+    b = W.c2_suite(index, 0, 20000, 0.1)
+    ref = O.solve_batch(b.problem_id, alg, b.u0)
+    got = gpu_solve(b.problem_id, alg, b.u0)
+    if klass(b.problem_id) == "exact":
+        check_against(ref, got, b.problem_id, np.zeros(len(b.u0), bool), f"C2 #{index} {alg}")
+    else:
+        agree = ((got["retcode"] == ref["retcode"]) & (got["nsteps"] == ref["nsteps"])).mean()
+        assert agree >= 0.97, f"C2 #{index} {alg}: retcode/nsteps agreement {agree:.4f}"
+
+
+@pytest.mark.parametrize("alg", ["broyden", "klement", "dfsane", "newton-raphson", "trust-region"])
+@pytest.mark.parametrize("n", [8, 16])
+def test_oracle_c3_c4_sample(n, alg):
+    from oracle import oracle as O
+    batches = [W.c3_rosenbrock(n, 0, 5000)] + ([W.c4_tridiagonal(0, 5000)] if n == 16 else [])
+    for b in batches:
+        ref = O.solve_batch(b.problem_id, alg, b.u0)
+        got = gpu_solve(b.problem_id, alg, b.u0)
+        check_against(ref, got, b.problem_id, np.zeros(len(b.u0), bool), f"{b.problem_id} {alg}")
+
+
+def test_c1_full_size_known_roots():
+    """1M parameter sets of u^2 - p: every solve succeeds and u = sqrt(p) to
+    rounding; the first 1024 are the reference's golden C1 systems."""
+    b = W.c1_quadratic(0, 1 << 20)
+    got = gpu_solve("quadratic", "newton-raphson", b.u0, b.p)
+    assert (got["retcode"] == 0).all()
+    assert (got["resid"] <= 1e-8).all()
+    assert close(got["u"], np.sqrt(b.p), 1e-12).all()
+    g = golden_case(next(c for c in CASES if c["case"] == "c1/newton-raphson"))
+    assert np.array_equal(bits(got["u"][:1024]), bits(g["u"]))
+    assert np.array_equal(got["nsteps"][:1024], g["nsteps"])
+
+
+def test_determinism_and_permutation_invariance():
+    b = W.c2_suite(23, 0, 200_000, 0.1)
+    a1 = gpu_solve(b.problem_id, "trust-region", b.u0)
+    a2 = gpu_solve(b.problem_id, "trust-region", b.u0)
+    for k in a1:
+        assert np.array_equal(a1[k], a2[k]), k
+    perm = np.random.default_rng(1).permutation(len(b.u0))
+    a3 = gpu_solve(b.problem_id, "trust-region", b.u0[perm])
+    assert np.array_equal(bits(a3["u"]), bits(a1["u"][perm]))
+    assert np.array_equal(a3["nsteps"], a1["nsteps"][perm])
+
+
+def test_host_buffer_path_equals_device_path():
+    import ctypes
+    b = W.c2_suite(13, 0, 300_001, 0.1)
+    dev = gpu_solve(b.problem_id, "newton-raphson", b.u0)
+    h, n, m = _lib.problem_lookup(b.problem_id, 10)
+    B = len(b.u0)
+    u0 = np.ascontiguousarray(b.u0.T)
+    uo = np.empty((n, B))
+    ro = np.empty(B)
+    rc = np.empty(B, np.int8)
+    cnt = np.empty((4, B), np.int32)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _lib.check(_lib.lib().nlk_solve_batch_host(h, 0, 0, B, ptr(u0), None, 1e-8, 1000, ptr(uo),
+                                               ptr(ro), ptr(rc), ptr(cnt[0]), ptr(cnt[1]),
+                                               ptr(cnt[2]), ptr(cnt[3]), 100_000, 3))
+    assert np.array_equal(bits(uo.T), bits(dev["u"]))
+    assert np.array_equal(rc, dev["retcode"])
+    assert np.array_equal(cnt[0], dev["nsteps"]) and np.array_equal(cnt[1], dev["nf"])
+
+
+@pytest.mark.parametrize("alg", ["newton-raphson", "trust-region", "klement", "dfsane"])
+def test_fp32_against_fp64(alg):
+    """fp32 has no reference; where fp32 and fp64 both succeed, u agrees to
+    1e-4 relative (north star), with abstol 1e-5 for fp32."""
+    b = W.c1_quadratic(0, 100_000, n=4, seed=5)
+    r64 = gpu_solve("quadratic", alg, b.u0, b.p)
+    r32 = gpu_solve("quadratic", alg, b.u0, b.p, abstol=1e-5, dtype=torch.float32)
+    both = (r64["retcode"] == 0) & (r32["retcode"] == 0)
+    assert both.mean() > 0.99
+    assert close(r32["u"][both], r64["u"][both], 1e-4).all()
+
+
+def test_drop_in_single_solve_and_polyalgorithm():
+    import paper_2403_16341_b200 as nlk
+    d = nlk.get_problem("test23/rosenbrock")
+    r = nlk.solve(d.problem, nlk.SimpleNewtonRaphson)
+    assert r.retcode is nlk.RetCode.SUCCESS and r.stats.nsteps == 2
+    r = nlk.run_preset("trust-region", d.problem)
+    assert r.success and r.stats.nsteps == 13
+    r = nlk.solve(d.problem)  # default poly-algorithm: NR succeeds first
+    assert r.success and r.stats.nsteps == 2
+    g = nlk.get_problem("generalized_rosenbrock?N=8")
+    r = nlk.run_preset("klement", g.problem)
+    assert r.retcode is nlk.RetCode.NONFINITE and r.stats.nsteps == 12
