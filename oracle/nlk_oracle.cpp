@@ -93,10 +93,13 @@ struct Ctx {
   int n;
   const double* p;
   int nf = 0, njac = 0, nlinsolve = 0, nsteps = 0;
+  int nudge = 0;  // +1/-1: move every float-residual component one ulp (sensitivity mask)
 
   void F(const double* u, double* f) {  // CountedResidual.at (core.py:119-123)
     nf += 1;
     prob->f(u, p, f, n);
+    if (nudge)
+      for (int i = 0; i < n; ++i) f[i] = std::nextafter(f[i], nudge > 0 ? INFINITY : -INFINITY);
   }
 };
 
@@ -485,8 +488,9 @@ static void dfsane(Ctx& c, const double* u0, double abstol, int maxiters, Result
 }
 
 static void solve_one(const ProblemDef* prob, int n, int alg, const double* u0, const double* p,
-                      double abstol, int maxiters, Result& r, int32_t* counters) {
+                      double abstol, int maxiters, int nudge, Result& r, int32_t* counters) {
   Ctx c;
+  c.nudge = nudge;
   c.prob = prob;
   c.n = n;
   c.p = p;
@@ -542,10 +546,12 @@ int oracle_jacobian(int h, int n, const double* x, const double* p, double* J) {
   return dense_jacobian(c, x, J) ? 1 : 0;
 }
 
-// Batched solve, AoS: u0 [B][n], p [B][m] (or null), u_out [B][n].
+// Batched solve, AoS: u0 [B][n], p [B][m] (or null), u_out [B][n].  nudge = +-1
+// perturbs every float residual by one ulp (the roundoff-sensitivity probe).
 int oracle_solve_batch(int h, int n, int alg, int64_t B, const double* u0, const double* p, int m,
                        double abstol, int maxiters, int nthreads, double* u_out, double* resid_out,
-                       int8_t* retcode, int32_t* nsteps, int32_t* nf, int32_t* njac, int32_t* nlinsolve) {
+                       int8_t* retcode, int32_t* nsteps, int32_t* nf, int32_t* njac, int32_t* nlinsolve,
+                       int nudge) {
   if (h < 0 || h >= kNumProblems || n < 1 || n > 16) return -1;
   if (alg < 0 || alg > 5) return -2;
   const ProblemDef* prob = &kProblems[h];
@@ -558,7 +564,7 @@ int oracle_solve_batch(int h, int n, int alg, int64_t B, const double* u0, const
       for (int64_t b = i; b < e; ++b) {
         Result r;
         int32_t cnt[4];
-        solve_one(prob, n, alg, u0 + b * n, p ? p + b * m : nullptr, abstol, maxiters, r, cnt);
+        solve_one(prob, n, alg, u0 + b * n, p ? p + b * m : nullptr, abstol, maxiters, nudge, r, cnt);
         for (int k = 0; k < n; ++k) u_out[b * n + k] = r.u[k];
         resid_out[b] = r.resid;
         retcode[b] = r.code;

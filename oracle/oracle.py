@@ -50,7 +50,7 @@ def lib():
         L.oracle_residual.argtypes = [c_int, c_int, dp, ctypes.c_void_p, dp]
         L.oracle_jacobian.argtypes = [c_int, c_int, dp, ctypes.c_void_p, dp]
         L.oracle_solve_batch.argtypes = [c_int, c_int, c_int, c_i64, dp, ctypes.c_void_p, c_int,
-                                         c_d, c_int, c_int, dp, dp, i8, ip, ip, ip, ip]
+                                         c_d, c_int, c_int, dp, dp, i8, ip, ip, ip, ip, c_int]
         L.oracle_ddot.restype = c_d
         L.oracle_ddot.argtypes = [c_int, dp, dp]
         L.oracle_gemv_A_x.argtypes = [c_int, dp, dp, dp]
@@ -93,8 +93,9 @@ def jacobian(problem_id, x, p=None, n=0):
     return J if ok else None
 
 
-def solve_batch(problem_id, alg, u0, p=None, abstol=1e-8, maxiters=1000, threads=None):
-    """Solve B systems (u0 [B, n], p [B, m]); returns a dict of arrays."""
+def solve_batch(problem_id, alg, u0, p=None, abstol=1e-8, maxiters=1000, threads=None, nudge=0):
+    """Solve B systems (u0 [B, n], p [B, m]); returns a dict of arrays.
+    nudge=+1/-1 moves every float residual one ulp up/down (sensitivity probe)."""
     u0 = np.ascontiguousarray(u0, dtype=np.float64)
     B, n = u0.shape
     h, nn, m = lookup(problem_id, n)
@@ -112,7 +113,18 @@ def solve_batch(problem_id, alg, u0, p=None, abstol=1e-8, maxiters=1000, threads
     rc = lib().oracle_solve_batch(h, n, ALGS[alg], B, u0, _pptr(p), m, float(abstol),
                                   int(maxiters), int(threads), out["u"], out["resid"],
                                   out["retcode"], out["nsteps"], out["nf"], out["njac"],
-                                  out["nlinsolve"])
+                                  out["nlinsolve"], int(nudge))
     if rc != 0:
         raise RuntimeError(f"oracle_solve_batch failed rc={rc}")
     return out
+
+
+def sensitivity_mask(problem_id, alg, u0, p=None, abstol=1e-8, maxiters=1000, base=None):
+    """Systems whose (retcode, nsteps) change when the float residual moves one
+    ulp in either direction — outcomes decided by roundoff."""
+    base = base or solve_batch(problem_id, alg, u0, p, abstol, maxiters)
+    mask = np.zeros(len(base["retcode"]), bool)
+    for d in (1, -1):
+        r = solve_batch(problem_id, alg, u0, p, abstol, maxiters, nudge=d)
+        mask |= (r["retcode"] != base["retcode"]) | (r["nsteps"] != base["nsteps"])
+    return mask
