@@ -39,14 +39,33 @@ template <class S> struct ScalarOf { using type = S; };
 template <int W, class T> struct ScalarOf<Dual<W, T>> { using type = T; };
 
 // ---- elementary functions of the float path ---------------------------------
-__device__ __forceinline__ double t_exp(double x) { return exp(x); }
-__device__ __forceinline__ float t_exp(float x) { return expf(x); }
-__device__ __forceinline__ double t_sin(double x) { return sin(x); }
-__device__ __forceinline__ float t_sin(float x) { return sinf(x); }
-__device__ __forceinline__ double t_cos(double x) { return cos(x); }
-__device__ __forceinline__ float t_cos(float x) { return cosf(x); }
-__device__ __forceinline__ double t_atan(double x) { return atan(x); }
-__device__ __forceinline__ float t_atan(float x) { return atanf(x); }
+// Out of line: a residual like test23/trigonometric makes ~60 of these calls
+// per iteration, and inlining each libdevice body blew the kernel up to
+// ~25k instructions (instruction-fetch stalls dominated, ncu).
+#ifndef NLK_INLINE_TRANS
+#define NLK_INLINE_TRANS 0
+#endif
+#if NLK_INLINE_TRANS
+#define NLK_TRANS_ATTR static __device__ __forceinline__
+#else
+#define NLK_TRANS_ATTR static __device__ __noinline__
+#endif
+NLK_TRANS_ATTR double nlk_exp(double x) { return exp(x); }
+NLK_TRANS_ATTR float nlk_exp(float x) { return expf(x); }
+NLK_TRANS_ATTR double nlk_sin(double x) { return sin(x); }
+NLK_TRANS_ATTR float nlk_sin(float x) { return sinf(x); }
+NLK_TRANS_ATTR double nlk_cos(double x) { return cos(x); }
+NLK_TRANS_ATTR float nlk_cos(float x) { return cosf(x); }
+NLK_TRANS_ATTR double nlk_atan(double x) { return atan(x); }
+NLK_TRANS_ATTR float nlk_atan(float x) { return atanf(x); }
+__device__ __forceinline__ double t_exp(double x) { return nlk_exp(x); }
+__device__ __forceinline__ float t_exp(float x) { return nlk_exp(x); }
+__device__ __forceinline__ double t_sin(double x) { return nlk_sin(x); }
+__device__ __forceinline__ float t_sin(float x) { return nlk_sin(x); }
+__device__ __forceinline__ double t_cos(double x) { return nlk_cos(x); }
+__device__ __forceinline__ float t_cos(float x) { return nlk_cos(x); }
+__device__ __forceinline__ double t_atan(double x) { return nlk_atan(x); }
+__device__ __forceinline__ float t_atan(float x) { return nlk_atan(x); }
 __device__ __forceinline__ double t_sqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ float t_sqrt(float x) { return sqrtf(x); }
 // Python `x ** 2` / `x ** 3` call glibc pow.  x*x is the correctly rounded

@@ -35,9 +35,12 @@ struct KernelArgs {
 };
 
 constexpr int kThreads = 128;
+#ifndef NLK_MIN_BLOCKS
+#define NLK_MIN_BLOCKS 1
+#endif
 
 template <class P, int N, class T, int ALG>
-__global__ void __launch_bounds__(kThreads) solve_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const KernelArgs a) {
   using Solver = typename SolverOf<P, N, T, ALG>::type;
   constexpr int M = P::M;
   const T* __restrict__ u0 = static_cast<const T*>(a.u0);
