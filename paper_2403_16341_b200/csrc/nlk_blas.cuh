@@ -20,19 +20,11 @@ namespace nlk {
 
 #define NLK_FD __device__ __forceinline__
 
-// Code-size policy.  Small systems (n <= 6) unroll every loop so vectors and
-// matrices stay in registers (the swaps below are predicated).  Larger
-// systems keep loops rolled: a fully unrolled n = 10 trust-region kernel is
-// ~25k SASS instructions (400 KB), which thrashes the instruction cache
-// (ncu: "no_instruction" is the top stall).  Rolled loops index local
-// memory, which stays L1-resident.
-#ifndef NLK_COMPACT_MIN
-#define NLK_COMPACT_MIN 99
-#endif
-template <int N> struct Tune {
-  static constexpr bool compact = N >= NLK_COMPACT_MIN;
-  static constexpr int unroll = compact ? 1 : 64;
-};
+// Every loop is fully unrolled (all sizes are template parameters), so
+// vectors and matrices stay in registers; data-dependent indices (pivots)
+// are applied with predicated swaps.  A rolled variant with local-memory
+// arrays was measured 2-5x slower (profiles/r01_variants_codegen.log).
+
 template <class T> NLK_FD T t_fma(T a, T b, T c) { return fma(a, b, c); }
 template <> NLK_FD float t_fma<float>(float a, float b, float c) { return fmaf(a, b, c); }
 
@@ -45,7 +37,7 @@ NLK_FD T ddot(const T* x, const T* y) {
     T v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) v[j] = T(0);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int b = 0; b < N16; b += 16) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -59,7 +51,7 @@ NLK_FD T ddot(const T* x, const T* y) {
     }
     s = (v[0] + v[2]) + (v[1] + v[3]);
   }
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = N16; i < N; ++i) s = t_fma(x[i], y[i], s);
   return s;
 }
@@ -67,13 +59,13 @@ template <int N, class T> NLK_FD T norm2(const T* x) { return sqrt(ddot<N, T>(x,
 
 // ---- GEMV-N column scheme (getf2 step 3 and `A.T @ x`) ---------------------
 // a(i, k) = A[OFF_R + i + (OFF_C + k) * LDA] (column-major storage).
-template <bool SUB, int NT, class T, class F>
+template <bool SUB, class T, class F>
 NLK_FD void gemv_n_scheme(const int M, const int NCOL, F a, const T* x, T* y) {
   const int M1 = M & ~3;
-#pragma unroll (Tune<NT>::unroll)
+#pragma unroll
   for (int i = 0; i < M1; ++i) {
     int k = 0;
-#pragma unroll (Tune<NT>::unroll)
+#pragma unroll
     for (; k + 4 <= NCOL; k += 4) {
       T t = a(i, k + 1) * x[k + 1];
       t = t_fma(a(i, k), x[k], t);
@@ -92,11 +84,11 @@ NLK_FD void gemv_n_scheme(const int M, const int NCOL, F a, const T* x, T* y) {
       y[i] = SUB ? y[i] - t : y[i] + t;
     }
   }
-#pragma unroll (Tune<NT>::unroll)
+#pragma unroll
   for (int i = M1; i < M; ++i) {
     if (NCOL == 0) continue;
     T t = T(0);
-#pragma unroll (Tune<NT>::unroll)
+#pragma unroll
     for (int k = 0; k < NCOL; ++k) t = t_fma(a(i, k), x[k], t);
     y[i] = SUB ? y[i] - t : y[i] + t;
   }
@@ -105,9 +97,9 @@ NLK_FD void gemv_n_scheme(const int M, const int NCOL, F a, const T* x, T* y) {
 // y = A.T @ x, A column-major N x N (A[i + j*N] = A_ij)
 template <int N, class T>
 NLK_FD void gemv_AT_x(const T* A, const T* x, T* y) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = 0; i < N; ++i) y[i] = T(0);
-  gemv_n_scheme<false, N>(N, N, [&](int i, int k) { return A[k + i * N]; }, x, y);
+  gemv_n_scheme<false>(N, N, [&](int i, int k) { return A[k + i * N]; }, x, y);
 }
 
 // y = A @ x (dgemv_t: 4x4 / 4x2 / 4x1 kernels + column tail), A col-major
@@ -118,14 +110,14 @@ NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
   if constexpr (N4 > 0) {
     if (row < N4) {
       T v[4] = {T(0), T(0), T(0), T(0)};
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int k = 0; k < N4; k += 4)
 #pragma unroll
         for (int l = 0; l < 4; ++l) v[l] = t_fma(A[row + (k + l) * N], x[k + l], v[l]);
       s = (v[0] + v[2]) + (v[1] + v[3]);
     } else if ((N & 2) && row < N4 + 2) {
       T v0 = T(0), v1 = T(0);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int k = 0; k < N4; k += 2) {
         v0 = v0 + A[row + k * N] * x[k];
         v1 = v1 + A[row + (k + 1) * N] * x[k + 1];
@@ -133,7 +125,7 @@ NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
       s = v0 + v1;
     } else {
  T v[4] = {T(0), T(0), T(0), T(0)};
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int k = 0; k < N4; k += 4)
 #pragma unroll
         for (int l = 0; l < 4; ++l) v[l] = v[l] + A[row + (k + l) * N] * x[k + l];
@@ -154,28 +146,20 @@ NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
 }
 template <int N, class T>
 NLK_FD void gemv_A_x(const T* A, const T* x, T* y) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = 0; i < N; ++i) y[i] = gemv_t_row<N>(i, A, x);
 }
 
 // ---- predicated swaps (data-dependent index, register-resident arrays) -----
 // swap v[i*S] <-> v[p*S] for p in (i, LIMIT)
-template <int LIMIT, int S, int NT, class T>
+template <int LIMIT, int S, class T>
 NLK_FD void swap_dyn(T* v, int i, int p) {
-  if constexpr (Tune<NT>::compact) {
-    if (p != i) {
-      T t = v[i * S];
-      v[i * S] = v[p * S];
-      v[p * S] = t;
-    }
-  } else {
 #pragma unroll
-    for (int r = 0; r < LIMIT; ++r) {
-      if (r > i && r == p) {
-        T t = v[i * S];
-        v[i * S] = v[r * S];
-        v[r * S] = t;
-      }
+  for (int r = 0; r < LIMIT; ++r) {
+    if (r > i && r == p) {
+      T t = v[i * S];
+      v[i * S] = v[r * S];
+      v[r * S] = t;
     }
   }
 }
@@ -183,39 +167,39 @@ NLK_FD void swap_dyn(T* v, int i, int p) {
 // ---- GETF2 on an M x NC panel (column-major, leading dimension LDA) --------
 template <int M, int NC, int LDA, class T>
 NLK_FD void getf2_panel(T* A, int* piv) {
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
   for (int j = 0; j < NC; ++j) {
     T b[M];
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
     for (int i = 0; i < M; ++i) b[i] = A[i + j * LDA];
     // 1. earlier interchanges
-#pragma unroll (Tune<LDA>::unroll)
-    for (int i = 0; i < j && i < M; ++i) swap_dyn<M, 1, LDA>(b, i, piv[i]);
+#pragma unroll
+    for (int i = 0; i < j && i < M; ++i) swap_dyn<M, 1>(b, i, piv[i]);
     // 2. rows 1..j-1: b[i] -= sdot(L[i,0:i], b[0:i])
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
     for (int i = 1; i < j && i < M; ++i) {
       const int c4 = i & ~3;
       T t1 = T(0), t2 = T(0);
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
       for (int k = 0; k < c4; k += 4) {
         T m1 = A[i + k * LDA] * b[k], m2 = A[i + (k + 1) * LDA] * b[k + 1];
         T m3 = A[i + (k + 2) * LDA] * b[k + 2], m4 = A[i + (k + 3) * LDA] * b[k + 3];
         t1 = t1 + (m1 + m3);
         t2 = t2 + (m2 + m4);
       }
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
       for (int k = c4; k < i; ++k) t1 = t_fma(A[i + k * LDA], b[k], t1);
       b[i] = b[i] - (t1 + t2);
     }
     if (j < M) {
       // 3. rows j..M-1: GEMV-N update with the finished columns
       if (j >= 1)
-        gemv_n_scheme<true, LDA>(M - j, j,
+        gemv_n_scheme<true>(M - j, j,
             [&](int i, int k) { return A[(j + i) + k * LDA]; }, b, b + j);
       // 4. pivot: first index of max |b[j:]|
       int p = j;
       T best = fabs(b[j]);
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
       for (int i = j + 1; i < M; ++i) {
         T v = fabs(b[i]);
         if (v > best) { best = v; p = i; }
@@ -223,21 +207,21 @@ NLK_FD void getf2_panel(T* A, int* piv) {
       piv[j] = p;
       // 5. interchange + scale (subnormal pivots left unscaled, as OpenBLAS)
       T bp = b[j];
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
       for (int i = j + 1; i < M; ++i)
         if (i == p) bp = b[i];
       if (bp != T(0)) {
-#pragma unroll (Tune<LDA>::unroll)
-        for (int k = 0; k < j; ++k) swap_dyn<M, 1, LDA>(A + k * LDA, j, p);
-        swap_dyn<M, 1, LDA>(b, j, p);
+#pragma unroll
+        for (int k = 0; k < j; ++k) swap_dyn<M, 1>(A + k * LDA, j, p);
+        swap_dyn<M, 1>(b, j, p);
         if (fabs(b[j]) >= Num<T>::dbl_min) {
           T r = T(1) / b[j];
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
           for (int i = j + 1; i < M; ++i) b[i] = b[i] * r;
         }
       }
     }
-#pragma unroll (Tune<LDA>::unroll)
+#pragma unroll
     for (int i = 0; i < M; ++i) A[i + j * LDA] = b[i];
   }
 }
@@ -245,12 +229,12 @@ NLK_FD void getf2_panel(T* A, int* piv) {
 // C(MI x NJ) -= A(MI x KK) * B(KK x NJ): one FMA chain per element, then subtract
 template <int MI, int NJ, int KK, int LD, class T>
 NLK_FD void gemm_minus(const T* A, const T* B, T* C) {
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
   for (int i = 0; i < MI; ++i)
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
     for (int j = 0; j < NJ; ++j) {
       T acc = T(0);
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
       for (int k = 0; k < KK; ++k) acc = t_fma(A[i + k * LD], B[k + j * LD], acc);
       C[i + j * LD] = C[i + j * LD] - acc;
     }
@@ -263,12 +247,12 @@ NLK_FD void trsm_lt_blocks(const T* L, T* C) {
     constexpr int REM = M - KK;
     constexpr int BS = REM >= 16 ? 16 : (REM & 8) ? 8 : (REM & 4) ? 4 : (REM & 2) ? 2 : 1;
     if constexpr (KK > 0) gemm_minus<BS, NJ, KK, LD>(L + KK, C, C + KK);
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
     for (int i = 0; i < BS; ++i)
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
       for (int j = 0; j < NJ; ++j) {
         T bb = C[KK + i + j * LD];
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
         for (int k = i + 1; k < BS; ++k)
           C[KK + k + j * LD] = t_fma(-bb, L[(KK + k) + (KK + i) * LD], C[KK + k + j * LD]);
       }
@@ -285,13 +269,13 @@ NLK_FD void getrf_blocks(T* A, int* piv) {
     constexpr int BK = (MN - IS) < BLK ? (MN - IS) : BLK;
     int sub[BK];
     getrf_rec<M - IS, BK, LD>(A + IS + IS * LD, sub);
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
     for (int i = 0; i < BK; ++i) piv[IS + i] = sub[i] + IS;
     if constexpr (IS + BK < NC) {
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
       for (int j = IS + BK; j < NC; ++j)
-#pragma unroll (Tune<LD>::unroll)
-        for (int i = IS; i < IS + BK; ++i) swap_dyn<M, 1, LD>(A + j * LD, i, piv[i]);
+#pragma unroll
+        for (int i = IS; i < IS + BK; ++i) swap_dyn<M, 1>(A + j * LD, i, piv[i]);
       trsm_lt_blocks<BK, NC - IS - BK, LD, 0>(A + IS + IS * LD, A + IS + (IS + BK) * LD);
       if constexpr (IS + BK < M)
         gemm_minus<M - IS - BK, NC - IS - BK, BK, LD>(A + (IS + BK) + IS * LD,
@@ -307,10 +291,10 @@ NLK_FD void getrf_late_swaps(T* A, const int* piv) {
   constexpr int MN = M < NC ? M : NC;
   if constexpr (IS < MN) {
     constexpr int BK = (MN - IS) < BLK ? (MN - IS) : BLK;
-#pragma unroll (Tune<LD>::unroll)
+#pragma unroll
     for (int j = IS; j < IS + BK; ++j)
-#pragma unroll (Tune<LD>::unroll)
-      for (int i = IS + BK; i < MN; ++i) swap_dyn<M, 1, LD>(A + j * LD, i, piv[i]);
+#pragma unroll
+      for (int i = IS + BK; i < MN; ++i) swap_dyn<M, 1>(A + j * LD, i, piv[i]);
     getrf_late_swaps<M, NC, LD, IS + BK, BLK>(A, piv);
   }
 }
@@ -335,7 +319,7 @@ template <int N, class T>
 NLK_FD bool lu_factor(T* A, int* piv) {
   T anorm = T(0);
   bool nan = false;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = 0; i < N * N; ++i) {
     T a = fabs(A[i]);
     nan |= (a != a);
@@ -344,7 +328,7 @@ NLK_FD bool lu_factor(T* A, int* piv) {
   if (nan || anorm == T(0) || !isfinite(anorm)) return false;
   getrf_rec<N, N, N>(A, piv);
   bool zero = false, pnan = false;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = 0; i < N; ++i) {
     T d = fabs(A[i + i * N]);
     pnan |= (d != d);
@@ -356,16 +340,16 @@ NLK_FD bool lu_factor(T* A, int* piv) {
 // getrs (one RHS): row swaps, column-oriented FMA forward/back substitution
 template <int N, class T>
 NLK_FD void getrs(const T* LU, const int* piv, T* b) {
-#pragma unroll (Tune<N>::unroll)
-  for (int i = 0; i < N; ++i) swap_dyn<N, 1, N>(b, i, piv[i]);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
+  for (int i = 0; i < N; ++i) swap_dyn<N, 1>(b, i, piv[i]);
+#pragma unroll
   for (int i = 0; i < N; ++i)
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int r = i + 1; r < N; ++r) b[r] = t_fma(-b[i], LU[r + i * N], b[r]);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = N - 1; i >= 0; --i) {
     b[i] = b[i] / LU[i + i * N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int r = 0; r < i; ++r) b[r] = t_fma(-b[i], LU[r + i * N], b[r]);
   }
 }

@@ -14,7 +14,7 @@
 #pragma once
 #include <stdint.h>
 
-#include "nlk_solvers.cuh"
+#include "nlk_coop.cuh"
 
 namespace nlk {
 
@@ -97,10 +97,92 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const K
   }
 }
 
+// Cooperative variant (nlk_coop.cuh): a group of N lanes per system, 32/N
+// systems per warp; refills are claimed per group by its row-0 lane.
+template <class P, int N, class T, int ALG>
+__global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel_coop(const KernelArgs a) {
+  using Solver = typename CoopOf<P, N, T, ALG>::type;
+  using Shape = CoopShape<N>;
+  constexpr int M = P::M;
+  constexpr int WARPS = kThreads / 32;
+  __shared__ T tbuf[WARPS][Shape::SPW][N * Shape::LD];
+  const T* __restrict__ u0 = static_cast<const T*>(a.u0);
+  const T* __restrict__ pp = static_cast<const T*>(a.p);
+  T* __restrict__ uo = static_cast<T*>(a.u_out);
+  T* __restrict__ ro = static_cast<T*>(a.resid_out);
+  const T abstol = static_cast<T>(a.abstol);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t B = a.B;
+  const bool idle = lane >= Shape::LANES;
+  const int grp = idle ? 0 : lane / N;
+
+  Solver s;
+  s.g.base = grp * N;
+  s.g.row = lane - s.g.base;
+  s.g.mask = ((1u << N) - 1u) << s.g.base;
+  s.tbuf = &tbuf[warp][grp][0];
+  const int64_t groups_total = static_cast<int64_t>(gridDim.x) * WARPS * Shape::SPW;
+  int64_t sys = idle ? B : (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * Shape::SPW + grp;
+  bool fresh = true;
+  for (;;) {
+    const bool need = !idle && sys < 0;
+    const bool leader_need = need && s.g.row == 0;
+    const unsigned want = __ballot_sync(0xffffffffu, leader_need);
+    if (want) {
+      const int leader = __ffs(want) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned long long>(__popc(want)));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      int64_t mine = static_cast<int64_t>(groups_total + base + __popc(want & ((1u << lane) - 1u)));
+      mine = __shfl_sync(0xffffffffu, mine, idle ? lane : s.g.base);
+      if (need) {
+        sys = mine;
+        fresh = true;
+      }
+    }
+    const bool live = !idle && sys < B;
+    if (!__any_sync(0xffffffffu, live)) break;
+    if (!live) continue;
+    int st;
+    if (fresh) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) s.u[i] = u0[i * B + sys];
+#pragma unroll
+      for (int i = 0; i < M; ++i) s.p[i] = pp[i * B + sys];
+      st = s.init(abstol);
+      fresh = false;
+    } else {
+      st = s.step(abstol, a.maxiters);
+    }
+    if (st != RUNNING) {
+      // lane r writes component r; row 0 writes the scalars
+      T ur = s.u[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i)
+        if (i == s.g.row) ur = s.u[i];
+      uo[s.g.row * B + sys] = ur;
+      if (s.g.row == 0) {
+        ro[sys] = max_abs<N>(s.f);
+        a.retcode[sys] = static_cast<int8_t>(st);
+        if (a.nsteps) a.nsteps[sys] = s.nsteps;
+        if (a.nf) a.nf[sys] = s.nf;
+        if (a.njac) a.njac[sys] = s.njac;
+        if (a.nlinsolve) a.nlinsolve[sys] = s.nlinsolve;
+      }
+      sys = -1;
+    }
+  }
+}
+
 // Host-side launcher: persistent grid sized from the occupancy calculator.
 template <class P, int N, class T, int ALG>
 cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out) {
-  auto kern = solve_kernel<P, N, T, ALG>;
+  auto kern = [] {
+    if constexpr (UseCoop<N, ALG>::value) return solve_kernel_coop<P, N, T, ALG>;
+    else return solve_kernel<P, N, T, ALG>;
+  }();
+  constexpr int per_block_systems = UseCoop<N, ALG>::value ? (kThreads / 32) * CoopShape<N>::SPW : kThreads;
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -109,7 +191,7 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  int64_t want = (a.B + kThreads - 1) / kThreads;
+  int64_t want = (a.B + per_block_systems - 1) / per_block_systems;
   int64_t grid = static_cast<int64_t>(per_sm) * sms;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;

@@ -40,25 +40,25 @@ template <int N, class S> NLK_FD S np_sum(const S* x) {
   using T = typename ScalarOf<S>::type;
   if constexpr (IsDual<S>::value) {
     S r = x[0];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 1; i < N; ++i) r = r + x[i];
     return r;
   } else if constexpr (N < 8) {
     S r = K(0);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) r = r + x[i];
     return r;
   } else {
     S r[8];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = x[j];
     constexpr int NB = N - (N % 8);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 8; i < NB; i += 8)
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int j = 0; j < 8; ++j) r[j] = r[j] + x[i + j];
     S res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = NB; i < N; ++i) res = res + x[i];
     return res;
   }
@@ -67,12 +67,12 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
   using T = typename ScalarOf<S>::type;
   if constexpr (IsDual<S>::value) {
     S r = x[0];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 1; i < N; ++i) r = r * x[i];
     return r;
   } else {
     S r = K(1);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) r = r * x[i];
     return r;
   }
@@ -164,12 +164,12 @@ struct Watson {  // 84-109 (n = 2)
 struct Chebyquad {  // 112-129 (n = 2)
   static constexpr int N = 2, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int j = 0; j < N; ++j) {
       S t_cur = K(2.0) * x[j] - K(1.0);
       S scale = K(2.0) * t_cur;
       S t_prev = t_cur;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) {
         out[i] = (j == 0) ? K(0.0) + t_cur : out[i] + t_cur;
         S t_next = (i == 0) ? scale * t_cur - K(1.0) : scale * t_cur - t_prev;
@@ -177,7 +177,7 @@ struct Chebyquad {  // 112-129 (n = 2)
         t_cur = t_next;
       }
     }
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) {
       out[k] = out[k] / T(N);
       if ((k + 1) % 2 == 0) out[k] = out[k] + K(1.0) / (T((k + 1) * (k + 1)) - K(1.0));
@@ -188,7 +188,7 @@ struct BrownAlmostLinear {  // 132-139
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     S total = np_sum<N>(x);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N - 1; ++k) out[k] = x[k] + total - K(N + 1.0);
     out[N - 1] = np_prod<N>(x) - K(1.0);
   }
@@ -197,7 +197,7 @@ struct DiscreteBoundaryValue {  // 142-151
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     const T h = K(1.0) / T(N + 1);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) {
       T tk = T(k + 1) * h;
       S a = K(2.0) * x[k];
@@ -212,20 +212,20 @@ struct DiscreteIntegral {  // 154-168
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     const T h = K(1.0) / T(N + 1);
     T t[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int j = 0; j < N; ++j) t[j] = T(j + 1) * h;
     S cubes[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int j = 0; j < N; ++j) cubes[j] = t_pow3(x[j] + t[j] + K(1.0));
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) {
       S s1 = K(0.0) + t[0] * cubes[0];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int j = 1; j <= k; ++j) s1 = s1 + t[j] * cubes[j];
       S inner = (K(1.0) - t[k]) * s1;
       if (k + 1 < N) {
         S s2 = K(0.0) + (K(1.0) - t[k + 1 < N ? k + 1 : 0]) * cubes[k + 1 < N ? k + 1 : 0];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
         for (int j = k + 2; j < N; ++j) s2 = s2 + (K(1.0) - t[j]) * cubes[j];
         inner = inner + t[k] * s2;
       } else {
@@ -239,10 +239,10 @@ struct Trigonometric {  // 171-177
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     S c[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) c[k] = t_cos(x[k]);
     S cos_sum = np_sum<N>(c);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k)
       out[k] = T(N) - cos_sum + T(k + 1) * (K(1.0) - t_cos(x[k])) - t_sin(x[k]);
   }
@@ -251,11 +251,11 @@ struct VariablyDimensioned {  // 180-188
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     S w[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) w[k] = T(k + 1) * (x[k] - K(1.0));
     S s = np_sum<N>(w);
     S temp = s * (K(1.0) + K(2.0) * s * s);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) out[k] = x[k] - K(1.0) + T(k + 1) * temp;
   }
 };
@@ -263,7 +263,7 @@ template <int NN>
 struct BroydenTridiagonal {  // 191-198 (n-generic)
   static constexpr int N = NN, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) {
       S a = (K(3.0) - K(2.0) * x[k]) * x[k];
       a = (k > 0) ? a - x[k > 0 ? k - 1 : 0] : a - K(0.0);
@@ -275,13 +275,13 @@ struct BroydenTridiagonal {  // 191-198 (n-generic)
 struct BroydenBanded {  // 201-210
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int k = 0; k < N; ++k) {
       const int lo = k - 5 > 0 ? k - 5 : 0;
       const int hi = k + 2 < N ? k + 2 : N;
       S acc = x[0];
       bool first = true;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int j = lo; j < hi; ++j) {
         if (j == k) continue;
         S term = x[j] * (K(1.0) + x[j]);
@@ -304,9 +304,9 @@ struct MatrixSqrt2x2 {  // 213-220
 struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
   static constexpr int N = 9, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < 3; ++i)
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int j = 0; j < 3; ++j) {
         S r;
         if constexpr (IsDual<S>::value) {  // object matmul: first product, then adds
@@ -372,26 +372,26 @@ struct Chandrasekhar {  // 286-292
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     T mu[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) mu[i] = (T(i + 1) - K(0.5)) / T(N);
     const T c = K(0.9) / (K(2.0) * T(N));
     S y[N];
     if constexpr (IsDual<S>::value) {  // object matmul: first product, then adds
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) {
         y[i] = x[0] * (mu[i] / (mu[i] + mu[0]));
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
         for (int k = 1; k < N; ++k) y[i] = y[i] + x[k] * (mu[i] / (mu[i] + mu[k]));
       }
     } else {  // BLAS dgemv_t on the C-ordered A (column-major copy here)
       T A[N * N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int r = 0; r < N; ++r)
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
         for (int k = 0; k < N; ++k) A[r + k * N] = mu[r] / (mu[r] + mu[k]);
       gemv_A_x<N>(A, x, y);
     }
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) out[i] = x[i] - K(1.0) / (K(1.0) - c * y[i]);
   }
 };
@@ -402,7 +402,7 @@ struct GeneralizedRosenbrock {  // 363-368
   static constexpr int N = NN, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
     out[0] = K(1.0) - x[0];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 1; i < N; ++i) out[i] = K(10.0) * (x[i] - x[i - 1] * x[i - 1]);
   }
 };
@@ -410,7 +410,7 @@ template <int NN>
 struct Quadratic {  // 382-383: u * u - theta
   static constexpr int N = NN, M = NN;
   template <class S, class T> NLK_FD static void f(const S* x, const T* p, S* out) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];
   }
 };

@@ -27,7 +27,7 @@ enum Alg : int { ALG_NR = 0, ALG_TR = 1, ALG_BROYDEN = 2, ALG_KLEMENT = 3, ALG_D
 
 template <int N, class T> NLK_FD bool all_finite(const T* x) {
   bool ok = true;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = 0; i < N; ++i) ok &= isfinite(x[i]);
   return ok;
 }
@@ -35,7 +35,7 @@ template <int N, class T> NLK_FD bool all_finite(const T* x) {
 template <int N, class T> NLK_FD T max_abs(const T* x) {
   T m = fabs(x[0]);
   bool nan = (m != m);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
   for (int i = 1; i < N; ++i) {
     T a = fabs(x[i]);
     nan |= (a != a);
@@ -69,21 +69,21 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* J, bool& vals_ok, int& bad_col
     constexpr int SW = SweepWidth<N>::value;
     constexpr int W = (N - C0) < SW ? (N - C0) : SW;
     Dual<W, T> xd[N], out[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) {
       xd[i].v = u[i];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int j = 0; j < W; ++j) xd[i].d[j] = (i == C0 + j) ? T(1) : T(0);
     }
     P::template f<Dual<W, T>, T>(xd, p, out);
     if constexpr (C0 == 0) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) vals_ok &= isfinite(out[i].v);
     }
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int j = 0; j < W; ++j) {
       bool colok = true;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) {
         colok &= isfinite(out[i].d[j]);
         J[i + (C0 + j) * N] = out[i].d[j];
@@ -144,13 +144,13 @@ struct NewtonRaphson : Base<P, N, T> {
     if (B::jac(J) >= 0) return NONFINITE;
     T Jf[LS ? N * N : 1];
     if constexpr (LS) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N * N; ++i) Jf[i] = J[i];
     }
     if (!lu_factor<N>(J, piv)) return LINSOLVE_FAILED;
     B::nlinsolve += 1;
     T du[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) du[i] = -B::f[i];
     getrs<N>(J, piv, du);
     T alpha = T(1);
@@ -165,7 +165,7 @@ struct NewtonRaphson : Base<P, N, T> {
       bool ok = false;
 #pragma unroll 1
       for (int it = 0; it < 31; ++it) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
         for (int i = 0; i < N; ++i) un[i] = B::u[i] + alpha * du[i];
         B::F(un, fn);
         T value = T(0.5) * ddot<N>(fn, fn);
@@ -174,11 +174,11 @@ struct NewtonRaphson : Base<P, N, T> {
       }
       if (!ok) return LINESEARCH_FAILED;
     }
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) un[i] = B::u[i] + alpha * du[i];
     B::F(un, fn);
     if (!(all_finite<N>(un) && all_finite<N>(fn))) return NONFINITE;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) { B::u[i] = un[i]; B::f[i] = fn[i]; }
     B::nsteps += 1;
     if (converged<N>(B::f, abstol)) return SUCCESS;
@@ -206,11 +206,11 @@ struct TrustRegion : Base<P, N, T> {
   // dogleg_direction (descent.py:78-106)
   NLK_FD void dogleg(T* out) {
     T newton[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) newton[i] = -B::f[i];
     getrs<N>(LU, piv, newton);
     if (norm2<N>(newton) <= radius) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) out[i] = newton[i];
       return;
     }
@@ -220,30 +220,30 @@ struct TrustRegion : Base<P, N, T> {
     T gg = ddot<N>(g, g);
     T jj = ddot<N>(Jg, Jg);
     T t_star = gg / ((Num<T>::tiny > jj) ? Num<T>::tiny : jj);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) cauchy[i] = -t_star * g[i];
     T cnorm = norm2<N>(cauchy);
     if (cnorm >= radius) {
       T s = -(radius / sqrt(gg));
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) out[i] = s * g[i];
       return;
     }
     T d[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) d[i] = newton[i] - cauchy[i];
     T a = ddot<N>(d, d);
     T b = T(2) * ddot<N>(cauchy, d);
     T c = cnorm * cnorm - radius * radius;
     T tau = (-b + sqrt(b * b - T(4) * a * c)) / (T(2) * a);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) out[i] = cauchy[i] + tau * d[i];
   }
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
     if (!cached) {
       if (B::jac(J) >= 0) return NONFINITE;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N * N; ++i) LU[i] = J[i];
       if (!lu_factor<N>(LU, piv)) return LINSOLVE_FAILED;
       cached = true;
@@ -253,14 +253,14 @@ struct TrustRegion : Base<P, N, T> {
     dogleg(du);
     if (!all_finite<N>(du)) return LINSOLVE_FAILED;
     T ut[N], ft[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) ut[i] = B::u[i] + du[i];
     B::F(ut, ft);
     T rho;
     if (all_finite<N>(ft)) {  // tr_ratio (globalize.py:121-134)
       T Jdu[N], model[N];
       gemv_A_x<N>(J, du, Jdu);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) model[i] = B::f[i] + Jdu[i];
       T ff = ddot<N>(B::f, B::f);
       T actual = ff - ddot<N>(ft, ft);
@@ -282,7 +282,7 @@ struct TrustRegion : Base<P, N, T> {
       accept = false;
     }
     if (accept) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) { B::u[i] = ut[i]; B::f[i] = ft[i]; }
       B::nsteps += 1;
       cached = false;
@@ -305,10 +305,10 @@ struct QuasiNewton : Base<P, N, T> {
 
   NLK_FD void qn_init() {  // IDENTITY_INIT (quasinewton.py:66-94)
     if constexpr (DIAG) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) H[i] = T(1);
     } else {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N * N; ++i) H[i] = (i % N == i / N) ? T(1) : T(0);
     }
   }
@@ -330,24 +330,24 @@ struct QuasiNewton : Base<P, N, T> {
     B::k += 1;
     T du[N];
     if constexpr (DIAG) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) du[i] = -(B::f[i] / H[i]);
     } else {
       T Hf[N];
       gemv_A_x<N>(H, B::f, Hf);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) du[i] = -Hf[i];
     }
     B::nlinsolve += 1;
     T un[N], fn[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) un[i] = B::u[i] + T(1) * du[i];
     B::F(un, fn);
     if (!(all_finite<N>(un) && all_finite<N>(fn))) return NONFINITE;
     T nnew = norm2<N>(fn);
     bool merit_decreased = nnew < norm2<N>(B::f);
     T s[N], t[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) {
       s[i] = un[i] - B::u[i];
       t[i] = fn[i] - B::f[i];
@@ -382,7 +382,7 @@ struct QuasiNewton : Base<P, N, T> {
     } else {
       if constexpr (DIAG) {  // klement_update (quasinewton.py:152-168)
         T thresh = T(1e-9) * max_abs<N>(s);
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
         for (int i = 0; i < N; ++i) {
           if (fabs(s[i]) > thresh) H[i] = t[i] / s[i];
           if (fabs(H[i]) < T(1e-12)) H[i] = (H[i] >= T(0)) ? T(1e-12) : T(-1e-12);
@@ -393,10 +393,10 @@ struct QuasiNewton : Base<P, N, T> {
         gemv_AT_x<N>(H, s, sH);
         T denom = ddot<N>(s, Ht);
         if (!(fabs(denom) < T(1e-12) * norm2<N>(s) * norm2<N>(Ht))) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
           for (int i = 0; i < N; ++i) {
             T a = s[i] - Ht[i];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
             for (int j = 0; j < N; ++j) H[i + j * N] = H[i + j * N] + a * sH[j] / denom;
           }
         }
@@ -419,7 +419,7 @@ struct DFSane : Base<P, N, T> {
     int st = B::start(abstol);
     fnorm = ddot<N>(B::f, B::f);
     f0 = fnorm;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < MEM; ++i) hist[i] = fnorm;
     sigma = T(1);
     return st;
@@ -430,22 +430,22 @@ struct DFSane : Base<P, N, T> {
     T cl = as < T(1e-10) ? T(1e-10) : (as > T(1e10) ? T(1e10) : as);
     sigma = (sigma >= T(0)) ? cl : -cl;
     T d[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) d[i] = -sigma * B::f[i];
     T eta = f0 / (T(B::k) * T(B::k));
     T fbar = hist[0];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 1; i < MEM; ++i) fbar = hist[i] > fbar ? hist[i] : fbar;
     T ap = T(1), am = T(1);
     T ua[N], fa[N], na;
 #pragma unroll 1
     for (int ls = 0;; ++ls) {
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) ua[i] = B::u[i] + ap * d[i];
       B::F(ua, fa);
       T np_ = ddot<N>(fa, fa);
       if (np_ <= fbar + eta - T(1e-4) * (ap * ap) * fnorm) { na = np_; break; }
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
       for (int i = 0; i < N; ++i) ua[i] = B::u[i] - am * d[i];
       B::F(ua, fa);
       T nm = ddot<N>(fa, fa);
@@ -460,7 +460,7 @@ struct DFSane : Base<P, N, T> {
     }
     if (!(all_finite<N>(ua) && all_finite<N>(fa))) return NONFINITE;
     T s[N], y[N];
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < N; ++i) {
       s[i] = ua[i] - B::u[i];
       y[i] = fa[i] - B::f[i];
@@ -470,7 +470,7 @@ struct DFSane : Base<P, N, T> {
     fnorm = na;
     B::nsteps += 1;
     const int slot = B::k % MEM;
-#pragma unroll (Tune<N>::unroll)
+#pragma unroll
     for (int i = 0; i < MEM; ++i)
       if (i == slot) hist[i] = fnorm;
     if (converged<N>(B::f, abstol)) return SUCCESS;
