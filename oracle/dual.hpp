@@ -8,6 +8,8 @@
 #pragma once
 #include <cmath>
 
+#include "npexp.hpp"
+
 namespace oracle {
 
 constexpr int MAXW = 16;
@@ -149,12 +151,11 @@ inline Dual np_arctan(const Dual& a) {
 }
 
 // Float-path counterparts: numpy float64 scalar / array ufuncs.  numpy's
-// float64 sin/cos/arctan equal glibc's; numpy's SIMD exp differs from glibc
-// in the last bit on a few percent of inputs — the
-// oracle uses glibc and the parity tests account for it.
+// float64 sin/cos/arctan equal glibc's; numpy's exp is Intel SVML on the
+// reference host (npexp.hpp), not glibc.
 inline double pow2(double x) { return libm_pow(x, 2.0); }
 inline double pow3(double x) { return libm_pow(x, 3.0); }
-inline double np_exp(double x) { return libm_exp(x); }
+inline double np_exp(double x) { return svml_exp(x); }
 inline double np_sqrt(double x) { return std::sqrt(x); }
 inline double np_sin(double x) { return libm_sin(x); }
 inline double np_cos(double x) { return libm_cos(x); }

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include "nlk_glibc.cuh"
+
 namespace nlk {
 
 template <class T> struct Num;  // numeric constants per precision
@@ -38,10 +40,14 @@ struct Dual {
 template <class S> struct ScalarOf { using type = S; };
 template <int W, class T> struct ScalarOf<Dual<W, T>> { using type = T; };
 
-// ---- elementary functions of the float path ---------------------------------
+// ---- elementary functions --------------------------------------------------------
+// fp64: the reference host's own algorithms (nlk_glibc.cuh): glibc for
+// CPython's math module, numpy's sin/cos/arctan and `x ** n`; Intel SVML for
+// numpy's float64 exp (np.exp on the float path, math.exp on the dual path).
+// fp32: CUDA's single-precision functions (no reference exists for fp32).
 // Out of line: a residual like test23/trigonometric makes ~60 of these calls
-// per iteration, and inlining each libdevice body blew the kernel up to
-// ~25k instructions (instruction-fetch stalls dominated, ncu).
+// per iteration, and inlining each body blew the kernel up to ~25k
+// instructions (instruction-fetch stalls dominated, ncu).
 #ifndef NLK_INLINE_TRANS
 #define NLK_INLINE_TRANS 0
 #endif
@@ -50,16 +56,21 @@ template <int W, class T> struct ScalarOf<Dual<W, T>> { using type = T; };
 #else
 #define NLK_TRANS_ATTR static __device__ __noinline__
 #endif
-NLK_TRANS_ATTR double nlk_exp(double x) { return exp(x); }
+NLK_TRANS_ATTR double nlk_exp(double x) { return glibc::exp(x); }      // math.exp (Dual path)
+NLK_TRANS_ATTR double nlk_np_exp(double x) { return svml::exp(x); }   // np.exp on float64
 NLK_TRANS_ATTR float nlk_exp(float x) { return expf(x); }
-NLK_TRANS_ATTR double nlk_sin(double x) { return sin(x); }
+NLK_TRANS_ATTR double nlk_sin(double x) { return glibc::sin(x); }
 NLK_TRANS_ATTR float nlk_sin(float x) { return sinf(x); }
-NLK_TRANS_ATTR double nlk_cos(double x) { return cos(x); }
+NLK_TRANS_ATTR double nlk_cos(double x) { return glibc::cos(x); }
 NLK_TRANS_ATTR float nlk_cos(float x) { return cosf(x); }
-NLK_TRANS_ATTR double nlk_atan(double x) { return atan(x); }
+NLK_TRANS_ATTR double nlk_atan(double x) { return glibc::atan(x); }
+NLK_TRANS_ATTR double nlk_pow2(double x) { return glibc::pow_int<2>(x); }
+NLK_TRANS_ATTR double nlk_pow3(double x) { return glibc::pow_int<3>(x); }
 NLK_TRANS_ATTR float nlk_atan(float x) { return atanf(x); }
-__device__ __forceinline__ double t_exp(double x) { return nlk_exp(x); }
+__device__ __forceinline__ double t_exp(double x) { return nlk_np_exp(x); }
 __device__ __forceinline__ float t_exp(float x) { return nlk_exp(x); }
+__device__ __forceinline__ double t_exp_math(double x) { return nlk_exp(x); }
+__device__ __forceinline__ float t_exp_math(float x) { return nlk_exp(x); }
 __device__ __forceinline__ double t_sin(double x) { return nlk_sin(x); }
 __device__ __forceinline__ float t_sin(float x) { return nlk_sin(x); }
 __device__ __forceinline__ double t_cos(double x) { return nlk_cos(x); }
@@ -68,18 +79,11 @@ __device__ __forceinline__ double t_atan(double x) { return nlk_atan(x); }
 __device__ __forceinline__ float t_atan(float x) { return nlk_atan(x); }
 __device__ __forceinline__ double t_sqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ float t_sqrt(float x) { return sqrtf(x); }
-// Python `x ** 2` / `x ** 3` call glibc pow.  x*x is the correctly rounded
-// square; the cube is formed in double-double and rounded once, which is
-// the correctly rounded cube except in rare near-halfway cases.
-__device__ __forceinline__ double t_pow2(double x) { return x * x; }
+// Python `x ** 2` / `x ** 3` (numpy float64 scalars and CPython floats) call
+// glibc pow, which is not correctly rounded; Dual ** 2 is v*v (autodiff.py:133).
+__device__ __forceinline__ double t_pow2(double x) { return nlk_pow2(x); }
 __device__ __forceinline__ float t_pow2(float x) { return x * x; }
-__device__ __forceinline__ double t_pow3(double x) {
-  double hi = x * x;
-  double lo = fma(x, x, -hi);
-  double p = hi * x;
-  double e = fma(hi, x, -p);
-  return p + (e + lo * x);
-}
+__device__ __forceinline__ double t_pow3(double x) { return nlk_pow3(x); }
 __device__ __forceinline__ float t_pow3(float x) { return x * x * x; }
 
 // ---- Dual arithmetic (autodiff.py:66-154) ----------------------------------
@@ -169,7 +173,7 @@ NLK_D Dual<W, T> t_pow3(const Dual<W, T>& a) {
 }
 // elementary functions (autodiff.py:189-217)
 NLK_D Dual<W, T> t_exp(const Dual<W, T>& a) {
-  T e = t_exp(a.v);
+  T e = t_exp_math(a.v);  // Dual.exp calls math.exp (autodiff.py:25-26, 189-191)
   Dual<W, T> r; r.v = e;
 #pragma unroll
   for (int i = 0; i < W; ++i) r.d[i] = e * a.d[i];

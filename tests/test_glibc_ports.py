@@ -1,0 +1,91 @@
+"""The device ports of glibc's exp / pow / sin / cos / atan
+(paper_2403_16341_b200/csrc/nlk_glibc.cuh) compiled for the host with g++
+are bit-identical to the libm the reference calls, on random inputs across
+every branch (the same source is what the kernels run)."""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+CSRC = os.path.join(ROOT, "paper_2403_16341_b200", "csrc")
+SHIM = r'''
+#include "nlk_glibc.cuh"
+extern "C" {
+void g_exp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::exp(x[i]); }
+void g_npexp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::svml::exp(x[i]); }
+void g_sin(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::sin(x[i]); }
+void g_cos(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::cos(x[i]); }
+void g_atan(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::atan(x[i]); }
+void g_pow2(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::pow_int<2>(x[i]); }
+void g_pow3(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::pow_int<3>(x[i]); }
+void l_exp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = ::exp(x[i]); }
+void l_sin(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = ::sin(x[i]); }
+void l_cos(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = ::cos(x[i]); }
+void l_atan(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = ::atan(x[i]); }
+void l_pow2(const double* x, double* y, long n) { double (*volatile p)(double, double) = ::pow; for (long i = 0; i < n; ++i) y[i] = p(x[i], 2.0); }
+void l_pow3(const double* x, double* y, long n) { double (*volatile p)(double, double) = ::pow; for (long i = 0; i < n; ++i) y[i] = p(x[i], 3.0); }
+}
+'''
+
+
+@pytest.fixture(scope="module")
+def lib(tmp_path_factory):
+    d = tmp_path_factory.mktemp("glibc")
+    src, so = d / "shim.cpp", d / "shim.so"
+    src.write_text(SHIM)
+    subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-builtin", "-shared",
+                    "-fPIC", "-I", CSRC, str(src), "-o", str(so), "-lm"], check=True)
+    L = ctypes.CDLL(str(so))
+    return L
+
+
+def inputs(kind, n, rng):
+    u = rng.uniform(-1, 1, n)
+    if kind == "exp":
+        parts = [u * 20, u * 745, u * 1e-3, rng.uniform(-1, 1, n) * 700]
+    elif kind in ("sin", "cos"):
+        parts = [u * 10, u * 3, u * 1e5, u * 1e-3, u * np.exp(rng.uniform(-18, 18, n))]
+    elif kind == "atan":
+        parts = [u, u * 20, u * 0.07, u * np.exp(rng.uniform(-40, 40, n))]
+    else:
+        parts = [u * 10, u * np.exp(rng.uniform(-300, 300, n)), u * 1e-310, 1 + u * 1e-6]
+    x = np.concatenate(parts + [np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, -1.0])])
+    return np.ascontiguousarray(x)
+
+
+@pytest.mark.parametrize("fn", ["exp", "sin", "cos", "atan", "pow2", "pow3"])
+def test_port_is_bit_exact(lib, fn):
+    rng = np.random.default_rng({"exp": 1, "sin": 2, "cos": 3, "atan": 4, "pow2": 5, "pow3": 6}[fn])
+    x = inputs(fn.rstrip("23"), 250_000, rng)
+    a, b = np.empty_like(x), np.empty_like(x)
+    ptr = lambda v: v.ctypes.data_as(ctypes.c_void_p)
+    getattr(lib, "g_" + fn)(ptr(x), ptr(a), ctypes.c_long(len(x)))
+    getattr(lib, "l_" + fn)(ptr(x), ptr(b), ctypes.c_long(len(x)))
+    same = (a.view(np.int64) == b.view(np.int64)) | (np.isnan(a) & np.isnan(b))
+    assert same.all(), f"{fn}: {np.count_nonzero(~same)} mismatches, e.g. x={x[~same][:3]}"
+
+
+def _numpy_uses_svml_exp():
+    try:
+        from numpy._core._multiarray_umath import __cpu_features__ as f
+    except ImportError:
+        return False
+    return bool(f.get("AVX512_SKX"))
+
+
+@pytest.mark.skipif(not _numpy_uses_svml_exp(), reason="numpy dispatches exp to SVML only on AVX512_SKX")
+def test_numpy_exp_port_is_bit_exact(lib):
+    """np.exp on this host is Intel SVML (__svml_exp8_ha), not glibc."""
+    rng = np.random.default_rng(7)
+    x = np.ascontiguousarray(np.concatenate([rng.uniform(-20, 20, 200_000),
+                                             rng.uniform(-707, 707, 200_000),
+                                             rng.uniform(-1e-6, 1e-6, 50_000)]))
+    a = np.empty_like(x)
+    lib.g_npexp(x.ctypes.data_as(ctypes.c_void_p), a.ctypes.data_as(ctypes.c_void_p),
+                ctypes.c_long(len(x)))
+    assert np.array_equal(a.view(np.int64), np.exp(x).view(np.int64))
