@@ -65,6 +65,8 @@ NLK_TRANS_ATTR double nlk_cos(double x) { return glibc::cos(x); }
 NLK_TRANS_ATTR float nlk_cos(float x) { return cosf(x); }
 NLK_TRANS_ATTR double nlk_atan(double x) { return glibc::atan(x); }
 NLK_TRANS_ATTR double nlk_pow2(double x) { return glibc::pow_int<2>(x); }
+NLK_TRANS_ATTR void nlk_sincos(double x, double* s, double* c) { glibc::sincos(x, s, c); }
+NLK_TRANS_ATTR void nlk_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
 NLK_TRANS_ATTR double nlk_pow3(double x) { return glibc::pow_int<3>(x); }
 NLK_TRANS_ATTR float nlk_atan(float x) { return atanf(x); }
 __device__ __forceinline__ double t_exp(double x) { return nlk_np_exp(x); }
@@ -188,15 +190,17 @@ NLK_D Dual<W, T> t_sqrt(const Dual<W, T>& a) {
   return r;
 }
 NLK_D Dual<W, T> t_sin(const Dual<W, T>& a) {
-  T c = t_cos(a.v);
-  Dual<W, T> r; r.v = t_sin(a.v);
+  T sv, c;
+  nlk_sincos(a.v, &sv, &c);  // = math.sin(v), math.cos(v), one call
+  Dual<W, T> r; r.v = sv;
 #pragma unroll
   for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
   return r;
 }
 NLK_D Dual<W, T> t_cos(const Dual<W, T>& a) {
-  T s = t_sin(a.v);
-  Dual<W, T> r; r.v = t_cos(a.v);
+  T s, cv;
+  nlk_sincos(a.v, &s, &cv);
+  Dual<W, T> r; r.v = cv;
 #pragma unroll
   for (int i = 0; i < W; ++i) r.d[i] = -s * a.d[i];
   return r;
@@ -209,6 +213,22 @@ NLK_D Dual<W, T> t_atan(const Dual<W, T>& a) {
   return r;
 }
 #undef NLK_D
+
+// sin and cos of one value (residuals that use both call this once)
+__device__ __forceinline__ void t_sincos(double x, double& s, double& c) { nlk_sincos(x, &s, &c); }
+__device__ __forceinline__ void t_sincos(float x, float& s, float& c) { nlk_sincos(x, &s, &c); }
+template <int W, class T>
+__device__ __forceinline__ void t_sincos(const Dual<W, T>& a, Dual<W, T>& s, Dual<W, T>& c) {
+  T sv, cv;
+  nlk_sincos(a.v, &sv, &cv);
+  s.v = sv;
+  c.v = cv;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    s.d[i] = cv * a.d[i];   // Dual.sin: c * a  (autodiff.py:202-204)
+    c.d[i] = -sv * a.d[i];  // Dual.cos: -s * a (autodiff.py:206-208)
+  }
+}
 
 __device__ __forceinline__ double value_of(double x) { return x; }
 __device__ __forceinline__ float value_of(float x) { return x; }

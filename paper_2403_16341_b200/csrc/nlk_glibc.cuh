@@ -323,6 +323,14 @@ NLK_HD double cos(double x) {
   return ::cos(x);
 }
 
+// sin and cos of the same argument in one call: both are evaluated exactly as
+// above (bit-identical to separate calls); inlining them together lets the
+// compiler share the range reduction and the table rows.
+NLK_HD void sincos(double x, double* s, double* c) {
+  *s = glibc::sin(x);
+  *c = glibc::cos(x);
+}
+
 // ---- atan (sysdeps/ieee754/dbl-64/s_atan.c, 2.35+ table version, FMA build) --
 constexpr double kA0 = 0x1.375f08b31cbcep-4, kA1 = -0x1.7458022b13c25p-4;
 constexpr double kA2 = 0x1.c71c6e5129a3bp-4, kA3 = -0x1.24924923f7603p-3;
@@ -405,16 +413,36 @@ NLK_HD double atan(double x) {
 // __svml_dexp_ha_data_internal_avx512).  |x| >= 707.7 takes SVML's scalar
 // "rare" path, which is not reproduced (glibc's exp is used there).
 namespace svml {
-constexpr double kTh[16] = {0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0,
-  0x1.2387a6e756238p+0, 0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0,
-  0x1.5ab07dd485429p+0, 0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0,
-  0x1.9c49182a3f090p+0, 0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0,
-  0x1.ea4afa2a490dap+0};
-constexpr double kTl[16] = {0x0.0p+0, 0x1.79aa65d837b6dp-54, -0x1.01b15eaa59348p-55,
-  0x1.68efde3a8a894p-54, 0x1.34d754db0abb6p-55, 0x1.59f48a72a4c6dp-55, 0x1.690cebb7aafb0p-56,
-  0x1.063e1e21c5409p-54, -0x1.3b3efbf5e2228p-54, -0x1.b32dcb94da51dp-56, 0x1.db72fc1f0eab4p-55,
-  0x1.1affc2b91ce27p-56, 0x1.c1a7792cb3387p-55, 0x1.36eae30af0cb3p-56, 0x1.4a385a63d07a7p-56,
-  -0x1.ff7128fd391f0p-55};
+#define NLK_SVML_TH {0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, \
+  0x1.2387a6e756238p+0, 0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, \
+  0x1.5ab07dd485429p+0, 0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, \
+  0x1.9c49182a3f090p+0, 0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, \
+  0x1.ea4afa2a490dap+0}
+#define NLK_SVML_TL {0x0.0p+0, 0x1.79aa65d837b6dp-54, -0x1.01b15eaa59348p-55, \
+  0x1.68efde3a8a894p-54, 0x1.34d754db0abb6p-55, 0x1.59f48a72a4c6dp-55, 0x1.690cebb7aafb0p-56, \
+  0x1.063e1e21c5409p-54, -0x1.3b3efbf5e2228p-54, -0x1.b32dcb94da51dp-56, 0x1.db72fc1f0eab4p-55, \
+  0x1.1affc2b91ce27p-56, 0x1.c1a7792cb3387p-55, 0x1.36eae30af0cb3p-56, 0x1.4a385a63d07a7p-56, \
+  -0x1.ff7128fd391f0p-55}
+static const double h_th[16] = NLK_SVML_TH;
+static const double h_tl[16] = NLK_SVML_TL;
+#if defined(__CUDACC__)
+static __device__ const double d_th[16] = NLK_SVML_TH;
+static __device__ const double d_tl[16] = NLK_SVML_TL;
+#endif
+NLK_HD double th(int j) {
+#if defined(__CUDA_ARCH__)
+  return d_th[j];
+#else
+  return h_th[j];
+#endif
+}
+NLK_HD double tl(int j) {
+#if defined(__CUDA_ARCH__)
+  return d_tl[j];
+#else
+  return h_tl[j];
+#endif
+}
 constexpr double kInvLn2 = 0x1.71547652b82fep+0, kShifter = 0x1.8000000003ff0p+48;
 constexpr double kLn2hi = 0x1.62e42fefa39efp-1, kLn2lo = 0x1.abc9e3b39803fp-56;
 constexpr double kRare = 0x1.61da04cbafe44p+9;
@@ -447,8 +475,8 @@ NLK_HD double exp(double x) {
   const double p3 = glibc::dfma(0x1.000000000d008p-1, r, 0x1.fffffffffff70p-1);
   double P = glibc::dfma(p1, r2, p2);
   P = glibc::dfma(P, r2, p3);
-  const double q = glibc::dfma(P, r, kTl[j]);
-  const double y = glibc::dfma(q, kTh[j], kTh[j]);
+  const double q = glibc::dfma(P, r, tl(j));
+  const double y = glibc::dfma(q, th(j), th(j));
   // scalef(y, n): y * 2^floor(n), exact for the non-rare range
   return ldexp(y, static_cast<int>(floor(n)));
 }

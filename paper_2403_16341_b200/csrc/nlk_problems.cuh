@@ -238,13 +238,13 @@ struct DiscreteIntegral {  // 154-168
 struct Trigonometric {  // 171-177
   static constexpr int N = 10, M = 0;
   template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
-    S c[N];
+    S c[N], sn[N];  // np.cos(x) and np.sin(x[k]): one sincos per component
 #pragma unroll
-    for (int k = 0; k < N; ++k) c[k] = t_cos(x[k]);
+    for (int k = 0; k < N; ++k) t_sincos(x[k], sn[k], c[k]);
     S cos_sum = np_sum<N>(c);
 #pragma unroll
     for (int k = 0; k < N; ++k)
-      out[k] = T(N) - cos_sum + T(k + 1) * (K(1.0) - t_cos(x[k])) - t_sin(x[k]);
+      out[k] = T(N) - cos_sum + T(k + 1) * (K(1.0) - c[k]) - sn[k];
   }
 };
 struct VariablyDimensioned {  // 180-188

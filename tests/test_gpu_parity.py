@@ -3,28 +3,17 @@
 Three layers, all on identical inputs:
   1. golden fixtures produced by the unmodified reference (small samples of
      every BASELINE.json config, all five algorithms + newton-backtracking);
-  2. the oracle restatement at larger samples (20k systems per C2 problem);
+  2. the oracle restatement at larger samples (20k systems per C2 problem,
+     5k per C3/C4 case);
   3. size-independent properties at full size (1M systems): known roots,
      determinism, permutation invariance, host-buffer path == device path.
 
-Arithmetic classes:
-  EXACT  only + - * / sqrt and BLAS/LAPACK models: every output bit-identical
-         to the reference, counters included — even on roundoff-sensitive
-         systems, because the rounding sequence is the same;
-  POW    Python `x**2`/`x**3` (glibc pow, not correctly rounded in ~0.1% of
-         cases; the device rounds x^2, x^3 correctly): retcode/nsteps exact
-         outside the sensitivity mask (<= 0.2 % slack), resid <= abstol on
-         success;
-  TRANS  exp/sin/cos/atan (numpy SIMD exp, glibc vs CUDA libdevice last
-         bits): retcode/nsteps exact outside the mask (<= 1 % slack for
-         multi-ulp flips the one-ulp probe cannot see), resid <= abstol on
-         success.
-  For POW/TRANS, u is not gated: these problems have degenerate or
-  ill-conditioned roots (double root, singular Jacobian at the root, badly
-  scaled), where a last-bit difference moves u by up to sqrt(abstol).
-The sensitivity mask is the reference's (golden fixtures) or the oracle's
-(larger samples): systems whose outcome flips under a one-ulp nudge of the
-float residual.
+Gate: bit-identical u and resid, and identical retcode, nsteps, nf, njac,
+nlinsolve, on every system — including the roundoff-sensitive ones (the
+survey's one-ulp probe flips up to 60 % of test23/trigonometric starts).
+This holds because the kernels reproduce the reference host's arithmetic:
+unfused residuals, the OpenBLAS/LAPACK operation orders, glibc's exp / pow /
+sin / cos / atan and numpy's SVML exp (nlk_glibc.cuh).
 """
 
 import numpy as np
@@ -36,16 +25,7 @@ from paper_2403_16341_b200 import _lib, solvers, workloads as W
 
 pytestmark = pytest.mark.gpu
 
-POW = {"test23/powell-singular", "test23/wood", "test23/double-root-scalar",
-       "test23/discrete-boundary-value", "test23/discrete-integral"}
-TRANS = {"test23/powell-badly-scaled", "test23/helical-valley", "test23/trigonometric",
-         "test23/dennis-schnabel", "test23/product-exponential", "test23/boggs"}
-
 CASES = load_manifest()["cases"]
-
-
-def klass(pid):
-    return "trans" if pid in TRANS else ("pow" if pid in POW else "exact")
 
 
 def gpu_solve(pid, alg, u0, p=None, abstol=1e-8, maxiters=1000, dtype=torch.float64):
@@ -58,21 +38,25 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
 
 
-def check_against(ref, got, pid, mask, what):
-    same = (got["retcode"] == ref["retcode"]) & (got["nsteps"] == ref["nsteps"])
-    k = klass(pid)
-    if k == "exact":
-        assert same.all(), f"{what}: retcode/nsteps differ at {np.nonzero(~same)[0][:10]}"
-        for c in ("nf", "njac", "nlinsolve"):
-            assert np.array_equal(got[c], ref[c]), f"{what}: {c}"
-        assert np.array_equal(bits(got["u"]), bits(ref["u"])), f"{what}: u bits"
-        assert np.array_equal(bits(got["resid"]), bits(ref["resid"])), f"{what}: resid bits"
-        return
-    bad = ~same & ~mask
-    slack = max(1, int(0.01 * (~mask).sum())) if k == "trans" else max(1, int(0.002 * len(same)))
-    assert bad.sum() <= slack, f"{what}: {bad.sum()} unmasked retcode/nsteps mismatches"
-    succ = same & (ref["retcode"] == 0)
-    assert (got["resid"][succ] <= 1e-8).all()
+# Known gap: glibc's sin/cos reduce arguments |x| >= 105414350 with the
+# Payne-Hanek __branred, which the device does not reproduce (it falls back to
+# CUDA's sin/cos there).  Only diverging trajectories reach such arguments;
+# systems whose reference iterate ended beyond |u| > 3e7 on the sin/cos
+# problems are reported, not gated.
+TRIG_PROBLEMS = {"test23/trigonometric", "test23/boggs"}
+
+
+def check_against(ref, got, what, problem_id=None):
+    exempt = np.zeros(len(ref["retcode"]), bool)
+    if problem_id in TRIG_PROBLEMS:
+        exempt = np.abs(np.asarray(ref["u"])).max(axis=1) > 3e7
+    same = np.ones(len(exempt), bool)
+    for k in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        same &= got[k] == ref[k]
+    same &= (bits(got["u"]) == bits(ref["u"])).all(axis=1)
+    same &= bits(got["resid"]) == bits(ref["resid"])
+    bad = np.nonzero(~same & ~exempt)[0]
+    assert len(bad) == 0, f"{what}: {len(bad)} systems differ (e.g. {bad[:8]}); exempt {exempt.sum()}"
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["case"] for c in CASES])
@@ -80,7 +64,7 @@ def test_golden(case):
     g = golden_case(case)
     p = g["p"] if g["p"].shape[1] else None
     got = gpu_solve(case["problem_id"], case["alg"], g["u0"], p)
-    check_against(g, got, case["problem_id"], g["sensitive"], case["case"])
+    check_against(g, got, case["case"], case["problem_id"])
 
 
 @pytest.mark.parametrize("alg", ["newton-raphson", "trust-region"])
@@ -90,11 +74,7 @@ def test_oracle_c2_sample(index, alg):
     b = W.c2_suite(index, 0, 20000, 0.1)
     ref = O.solve_batch(b.problem_id, alg, b.u0)
     got = gpu_solve(b.problem_id, alg, b.u0)
-    if klass(b.problem_id) == "exact":
-        mask = np.zeros(len(b.u0), bool)
-    else:
-        mask = O.sensitivity_mask(b.problem_id, alg, b.u0, base=ref)
-    check_against(ref, got, b.problem_id, mask, f"C2 #{index} {alg}")
+    check_against(ref, got, f"C2 #{index} {alg}", b.problem_id)
 
 
 @pytest.mark.parametrize("alg", ["broyden", "klement", "dfsane", "newton-raphson", "trust-region"])
@@ -105,7 +85,7 @@ def test_oracle_c3_c4_sample(n, alg):
     for b in batches:
         ref = O.solve_batch(b.problem_id, alg, b.u0)
         got = gpu_solve(b.problem_id, alg, b.u0)
-        check_against(ref, got, b.problem_id, np.zeros(len(b.u0), bool), f"{b.problem_id} {alg}")
+        check_against(ref, got, f"{b.problem_id} {alg}", b.problem_id)
 
 
 def test_c1_full_size_known_roots():
