@@ -219,6 +219,9 @@ def run_ours(args, rank, world, local_rank, dist):
     B = args.batch
     lo, hi = rank * B, (rank + 1) * B
     jobs = jobs_for(args.config, lo, hi)
+    if args.only:
+        keys = args.only.split(",")
+        jobs = [j for j in jobs if any(k in f"{j[0]}:{j[2]}" for k in keys)]
 
     # device-resident SoA inputs (shared by the jobs of one problem) and outputs
     inputs, prepared = {}, []
@@ -370,6 +373,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=60, help="systems per job for the CPU leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats", default=None, help="write per-launch stats JSON here")
+    ap.add_argument("--only", default=None,
+                    help="comma-separated substrings: keep only matching (problem, algorithm) jobs "
+                         "(profiling aid; the default runs the whole workload)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

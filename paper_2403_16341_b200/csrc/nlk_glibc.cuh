@@ -323,10 +323,36 @@ NLK_HD double cos(double x) {
   return ::cos(x);
 }
 
-// sin and cos of the same argument in one call: both are evaluated exactly as
-// above (bit-identical to separate calls); inlining them together lets the
-// compiler share the range reduction and the table rows.
+// sin and cos of the same argument in one evaluation, each bit-identical to
+// glibc's separate sin() and cos(): the range split is shared, and where both
+// results reduce to the same table row (|x| < 0.855 and the reduced range)
+// the row is read once and both kernels are formed from it.
 NLK_HD void sincos(double x, double* s, double* c) {
+  const uint32_t k = static_cast<uint32_t>(asu(x) >> 32) & 0x7fffffffu;
+  if (k < 0x3feb6000u) {  // |x| < 0.855469
+    *s = (k < 0x3e500000u) ? x : (fabs(x) < kSmall ? taylor_sin(x, 0.0) : do_sin_tab(x, 0.0));
+    *c = (k < 0x3e400000u) ? 1.0 : do_cos_tab(x, 0.0);
+    return;
+  }
+  if (k < 0x400368fdu) {  // |x| < 2.426265
+    const double y = kHp0 - fabs(x);
+    *s = copysign(do_cos_tab(y, kHp1), x);
+    const double a = y + kHp1;
+    const double da = (y - a) + kHp1;
+    *c = do_sin(a, da);
+    return;
+  }
+  if (k < 0x419921fbu) {  // |x| < 105414350: reduce once, both from (a, da, n)
+    double a, da;
+    const int n = reduce_sincos(x, &a, &da);
+    const double vs = do_sin(a, da);
+    const double vc = do_cos_tab(a, da);
+    const double rs = (n & 1) ? vc : vs;
+    const double rc = ((n + 1) & 1) ? vc : vs;
+    *s = (n & 2) ? -rs : rs;
+    *c = ((n + 1) & 2) ? -rc : rc;
+    return;
+  }
   *s = glibc::sin(x);
   *c = glibc::cos(x);
 }

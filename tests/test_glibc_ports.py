@@ -17,6 +17,8 @@ SHIM = r'''
 #include "nlk_glibc.cuh"
 extern "C" {
 void g_exp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::exp(x[i]); }
+void g_sincos_s(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) { double c; nlk::glibc::sincos(x[i], &y[i], &c); } }
+void g_sincos_c(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) { double s; nlk::glibc::sincos(x[i], &s, &y[i]); } }
 void g_npexp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::svml::exp(x[i]); }
 void g_sin(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::sin(x[i]); }
 void g_cos(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::cos(x[i]); }
@@ -58,14 +60,16 @@ def inputs(kind, n, rng):
     return np.ascontiguousarray(x)
 
 
-@pytest.mark.parametrize("fn", ["exp", "sin", "cos", "atan", "pow2", "pow3"])
+@pytest.mark.parametrize("fn", ["exp", "sin", "cos", "atan", "pow2", "pow3", "sincos_s", "sincos_c"])
 def test_port_is_bit_exact(lib, fn):
-    rng = np.random.default_rng({"exp": 1, "sin": 2, "cos": 3, "atan": 4, "pow2": 5, "pow3": 6}[fn])
-    x = inputs(fn.rstrip("23"), 250_000, rng)
+    rng = np.random.default_rng({"exp": 1, "sin": 2, "cos": 3, "atan": 4, "pow2": 5, "pow3": 6, "sincos_s": 7, "sincos_c": 8}[fn])
+    kind = {"sincos_s": "sin", "sincos_c": "cos"}.get(fn, fn.rstrip("23"))
+    x = inputs(kind, 250_000, rng)
     a, b = np.empty_like(x), np.empty_like(x)
     ptr = lambda v: v.ctypes.data_as(ctypes.c_void_p)
     getattr(lib, "g_" + fn)(ptr(x), ptr(a), ctypes.c_long(len(x)))
-    getattr(lib, "l_" + fn)(ptr(x), ptr(b), ctypes.c_long(len(x)))
+    ref = {"sincos_s": "sin", "sincos_c": "cos"}.get(fn, fn)
+    getattr(lib, "l_" + ref)(ptr(x), ptr(b), ctypes.c_long(len(x)))
     same = (a.view(np.int64) == b.view(np.int64)) | (np.isnan(a) & np.isnan(b))
     assert same.all(), f"{fn}: {np.count_nonzero(~same)} mismatches, e.g. x={x[~same][:3]}"
 
