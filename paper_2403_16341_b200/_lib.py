@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnlk_b200.so")
+# NLK_LIB_PATH selects a variant build (python -m paper_2403_16341_b200.build --tag)
+LIB_PATH = os.environ.get("NLK_LIB_PATH") or os.path.join(_PKG, "libnlk_b200.so")
 
 NLK_OK = 0
 ERRORS = {

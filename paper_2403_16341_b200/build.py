@@ -45,13 +45,13 @@ def _newest_header():
     return max(os.path.getmtime(h) for h in hs) if hs else 0.0
 
 
-def _compile(src, force, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src, force, verbose, obj_dir=OBJ, defines=()):
+    obj = os.path.join(obj_dir, os.path.basename(src).replace(".cu", ".o"))
     log = obj.replace(".o", ".ptxas.log")
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), _newest_header())):
         return obj, None
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -62,20 +62,23 @@ def _compile(src, force, verbose):
     return obj, log
 
 
-def build(force=False, verbose=False, jobs=None):
-    os.makedirs(OBJ, exist_ok=True)
+def build(force=False, verbose=False, jobs=None, tag=None, defines=()):
+    """Compile and link; ``tag``/``defines`` make a variant library
+    ``libnlk_b200_<tag>.so`` (objects in ``_obj_<tag>``) for A/B timing."""
+    obj_dir, lib = (OBJ, LIB) if not tag else (OBJ + "_" + tag, LIB.replace(".so", f"_{tag}.so"))
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = jobs or os.cpu_count() or 4
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, force, verbose), srcs))
+        results = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, defines), srcs))
     objs = [o for o, _ in results]
-    if (force or not os.path.exists(LIB)
-            or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
-        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs]
+    if (force or not os.path.exists(lib)
+            or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
+        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    return LIB
+    return lib
 
 
 def main(argv=None):
@@ -83,8 +86,10 @@ def main(argv=None):
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("-j", "--jobs", type=int, default=None)
+    ap.add_argument("--tag", default=None, help="variant name (separate objects and .so)")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for nvcc")
     a = ap.parse_args(argv)
-    print(build(a.force, a.verbose, a.jobs))
+    print(build(a.force, a.verbose, a.jobs, a.tag, a.defines))
 
 
 if __name__ == "__main__":

@@ -34,7 +34,7 @@ struct KernelArgs {
   unsigned long long* counter;  // refills claimed so far (zeroed before launch)
 };
 
-constexpr int kThreads = 128;
+constexpr int kThreads = kSmStride;
 #ifndef NLK_MIN_BLOCKS
 #define NLK_MIN_BLOCKS 1
 #endif
@@ -52,6 +52,10 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const K
   const int64_t B = a.B;
 
   Solver s;
+  if constexpr (Solver::kSmemElems > 0) {
+    extern __shared__ __align__(16) unsigned char nlk_dyn_smem[];
+    s.sm = reinterpret_cast<T*>(nlk_dyn_smem) + threadIdx.x;
+  }
   // first assignment is static (one system per thread), refills are dynamic
   int64_t sys = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   bool fresh = true;
@@ -188,7 +192,15 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  size_t smem = 0;
+  if constexpr (!UseCoop<N, ALG>::value) {
+    smem = sizeof(T) * kThreads * SolverOf<P, N, T, ALG>::type::kSmemElems;
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t want = (a.B + per_block_systems - 1) / per_block_systems;
@@ -196,7 +208,7 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = static_cast<int>(grid);
-  kern<<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(a);
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,269 @@
+// Shared-memory LU for the larger systems (n >= NLK_SMEM_NR_MIN / _TR_MIN).
+//
+// The register-resident LU of nlk_blas.cuh applies row interchanges with
+// predicated swaps (a data-dependent pivot cannot index a register array):
+// at n = 9/10 that is O(n^3) selects, ~14k SASS instructions per kernel, the
+// kernels stall on instruction fetch and spill.  Here the matrix lives in a
+// per-thread slice of shared memory (element e of thread t at
+// smem[e * 128 + t]: consecutive lanes hit consecutive words, conflict-free).
+// Loops are fully unrolled, so every element address is an immediate offset
+// from the thread's slice base, and an interchange is two indexed loads and
+// stores instead of a select chain.  Measured on B200 (C2, B = 262144):
+// 740 ms -> 417 ms per step; rolled loops (NLK_SMEM_UNROLL=0) are smaller
+// but spend their issue slots on address arithmetic (736 ms).
+// The arithmetic is the same OpenBLAS getrf/GETF2/TRSM/GEMM + getrs operation
+// sequence as nlk_blas.cuh, element for element.
+#pragma once
+#include "nlk_blas.cuh"
+
+namespace nlk {
+
+// n thresholds for the shared-memory path, per driver
+#ifndef NLK_SMEM_NR_MIN
+#define NLK_SMEM_NR_MIN 9
+#endif
+#ifndef NLK_SMEM_TR_MIN
+#define NLK_SMEM_TR_MIN 9
+#endif
+// 1: unroll every loop (immediate smem offsets); 0: rolled loops
+#ifndef NLK_SMEM_UNROLL
+#define NLK_SMEM_UNROLL 1
+#endif
+#if NLK_SMEM_UNROLL
+#define NLK_SMU _Pragma("unroll")
+#else
+#define NLK_SMU _Pragma("unroll 1")
+#endif
+
+#define NLK_FD __device__ __forceinline__
+
+// threads per block of the solve kernel = stride of the per-thread slices
+constexpr int kSmStride = 128;
+
+// column-major N x N matrix in a strided per-thread shared-memory slice
+template <int N, class T>
+struct SMat {
+  T* base;
+  NLK_FD T& operator()(int i, int j) const { return base[(i + j * N) * kSmStride]; }
+  NLK_FD T& v(int i) const { return base[i * kSmStride]; }  // as a vector
+};
+
+template <int N, class T>
+NLK_FD void sm_swap_rows(const SMat<N, T>& A, int r1, int r2, int c0, int c1) {
+NLK_SMU
+  for (int k = c0; k < c1; ++k) {
+    T t = A(r1, k);
+    A(r1, k) = A(r2, k);
+    A(r2, k) = t;
+  }
+}
+
+// GETF2 on rows OFF..N-1, columns OFF..OFF+NC-1; piv holds absolute rows
+template <int N, class T>
+NLK_FD void sm_getf2(const SMat<N, T>& A, int OFF, int NC, int* piv) {
+  const int M = N - OFF;
+NLK_SMU
+  for (int j = 0; j < NC; ++j) {
+    const int c = OFF + j;
+    // 1. earlier interchanges of this panel, applied to column c
+NLK_SMU
+    for (int i = 0; i < j; ++i) {
+      const int p = piv[OFF + i];
+      if (p != OFF + i) { T t = A(OFF + i, c); A(OFF + i, c) = A(p, c); A(p, c) = t; }
+    }
+    // 2. rows 1..j-1: b_i -= sdot(L[i, 0:i], b[0:i])
+NLK_SMU
+    for (int i = 1; i < j; ++i) {
+      const int c4 = i & ~3;
+      T t1 = T(0), t2 = T(0);
+NLK_SMU
+      for (int k = 0; k < c4; k += 4) {
+        T m1 = A(OFF + i, OFF + k) * A(OFF + k, c);
+        T m2 = A(OFF + i, OFF + k + 1) * A(OFF + k + 1, c);
+        T m3 = A(OFF + i, OFF + k + 2) * A(OFF + k + 2, c);
+        T m4 = A(OFF + i, OFF + k + 3) * A(OFF + k + 3, c);
+        t1 = t1 + (m1 + m3);
+        t2 = t2 + (m2 + m4);
+      }
+NLK_SMU
+      for (int k = c4; k < i; ++k) t1 = t_fma(A(OFF + i, OFF + k), A(OFF + k, c), t1);
+      A(OFF + i, c) = A(OFF + i, c) - (t1 + t2);
+    }
+    if (j >= M) continue;
+    // 3. rows j..M-1: GEMV-N scheme with the j finished columns
+    if (j >= 1) {
+      const int MM = M - j, M1 = MM & ~3;
+NLK_SMU
+      for (int ii = 0; ii < MM; ++ii) {
+        const int r = OFF + j + ii;
+        T y = A(r, c);
+        if (ii < M1) {
+          int k = 0;
+NLK_SMU
+          for (; k + 4 <= j; k += 4) {
+            T t = A(r, OFF + k + 1) * A(OFF + k + 1, c);
+            t = t_fma(A(r, OFF + k), A(OFF + k, c), t);
+            t = t_fma(A(r, OFF + k + 2), A(OFF + k + 2, c), t);
+            t = t_fma(A(r, OFF + k + 3), A(OFF + k + 3, c), t);
+            y = y - t;
+          }
+          if (k + 2 <= j) {
+            T t = A(r, OFF + k + 1) * A(OFF + k + 1, c);
+            t = t_fma(A(r, OFF + k), A(OFF + k, c), t);
+            y = y - t;
+            k += 2;
+          }
+          if (k < j) y = y - A(r, OFF + k) * A(OFF + k, c);
+        } else {
+          T t = T(0);
+NLK_SMU
+          for (int k = 0; k < j; ++k) t = t_fma(A(r, OFF + k), A(OFF + k, c), t);
+          y = y - t;
+        }
+        A(r, c) = y;
+      }
+    }
+    // 4. pivot: first index of max |b[j:]|
+    int p = c;
+    T best = fabs(A(c, c));
+NLK_SMU
+    for (int r = c + 1; r < N; ++r) {
+      T v = fabs(A(r, c));
+      if (v > best) { best = v; p = r; }
+    }
+    piv[c] = p;
+    // 5. interchange over the finished panel columns and b, then scale
+    if (A(p, c) != T(0)) {
+      if (p != c) sm_swap_rows(A, c, p, OFF, c + 1);
+      const T bj = A(c, c);
+      if (fabs(bj) >= Num<T>::dbl_min) {
+        const T rr = T(1) / bj;
+NLK_SMU
+        for (int r = c + 1; r < N; ++r) A(r, c) = A(r, c) * rr;
+      }
+    }
+  }
+}
+
+// C(rows r0.., cols c0..) -= A(rows r0.., cols k0..k0+KK) * B(rows k0.., cols c0..)
+template <int N, class T>
+NLK_FD void sm_gemm_minus(const SMat<N, T>& A, int r0, int MI, int c0, int NJ, int k0, int KK) {
+NLK_SMU
+  for (int i = 0; i < MI; ++i)
+NLK_SMU
+    for (int j = 0; j < NJ; ++j) {
+      T acc = T(0);
+NLK_SMU
+      for (int k = 0; k < KK; ++k) acc = t_fma(A(r0 + i, k0 + k), A(k0 + k, c0 + j), acc);
+      A(r0 + i, c0 + j) = A(r0 + i, c0 + j) - acc;
+    }
+}
+
+// TRSM_LT (unit L) on rows IS..IS+BK-1, columns C0..N-1; sub-blocks follow
+// the bits of BK (BK <= 8 here, so no 16-blocks)
+template <int N, class T>
+NLK_FD void sm_trsm(const SMat<N, T>& A, int IS, int BK) {
+  const int C0 = IS + BK, NJ = N - C0;
+  int kk = 0;
+NLK_SMU
+  for (int bs = 8; bs >= 1; bs >>= 1) {
+    if (!(BK & bs)) continue;
+    if (kk > 0) sm_gemm_minus(A, IS + kk, bs, C0, NJ, IS, kk);
+NLK_SMU
+    for (int i = 0; i < bs; ++i)
+NLK_SMU
+      for (int j = 0; j < NJ; ++j) {
+        const T bb = A(IS + kk + i, C0 + j);
+NLK_SMU
+        for (int k = i + 1; k < bs; ++k)
+          A(IS + kk + k, C0 + j) = t_fma(-bb, A(IS + kk + k, IS + kk + i), A(IS + kk + k, C0 + j));
+      }
+    kk += bs;
+  }
+}
+
+template <int N, class T>
+NLK_FD void sm_getrf(const SMat<N, T>& A, int* piv) {
+  constexpr int BLK = ((N / 2 + 1) / 2) * 2;
+  if constexpr (BLK <= 4) {
+    sm_getf2(A, 0, N, piv);
+  } else {
+NLK_SMU
+    for (int is = 0; is < N; is += BLK) {
+      const int bk = (N - is) < BLK ? (N - is) : BLK;
+      sm_getf2(A, is, bk, piv);  // panels of n <= 16 are always GETF2
+      if (is + bk < N) {
+NLK_SMU
+        for (int i = is; i < is + bk; ++i)
+          if (piv[i] != i) sm_swap_rows(A, i, piv[i], is + bk, N);
+        sm_trsm(A, is, bk);
+        sm_gemm_minus(A, is + bk, N - is - bk, is + bk, N - is - bk, is, bk);
+      }
+    }
+NLK_SMU
+    for (int is = 0; is < N; is += BLK) {
+      const int bk = (N - is) < BLK ? (N - is) : BLK;
+NLK_SMU
+      for (int i = is + bk; i < N; ++i)
+        if (piv[i] != i) sm_swap_rows(A, i, piv[i], is, is + bk);
+    }
+  }
+}
+
+template <int N, class T>
+NLK_FD bool sm_lu_factor(const SMat<N, T>& A, int* piv) {
+  T anorm = T(0);
+  bool nan = false;
+NLK_SMU
+  for (int e = 0; e < N * N; ++e) {
+    const T a = fabs(A.v(e));
+    nan |= (a != a);
+    anorm = a > anorm ? a : anorm;
+  }
+  if (nan || anorm == T(0) || !isfinite(anorm)) return false;
+  sm_getrf(A, piv);
+  bool zero = false, pnan = false;
+NLK_SMU
+  for (int i = 0; i < N; ++i) {
+    const T d = fabs(A(i, i));
+    pnan |= (d != d);
+    zero |= (d <= T(0));
+  }
+  return pnan || !zero;
+}
+
+// getrs with the right-hand side in the strided vector b (N elements)
+template <int N, class T>
+NLK_FD void sm_getrs(const SMat<N, T>& LU, const int* piv, const SMat<N, T>& b) {
+NLK_SMU
+  for (int i = 0; i < N; ++i) {
+    const int p = piv[i];
+    if (p != i) { T t = b.v(i); b.v(i) = b.v(p); b.v(p) = t; }
+  }
+NLK_SMU
+  for (int i = 0; i < N; ++i) {
+    const T bi = b.v(i);
+NLK_SMU
+    for (int r = i + 1; r < N; ++r) b.v(r) = t_fma(-bi, LU(r, i), b.v(r));
+  }
+NLK_SMU
+  for (int i = N - 1; i >= 0; --i) {
+    const T bi = b.v(i) / LU(i, i);
+    b.v(i) = bi;
+NLK_SMU
+    for (int r = 0; r < i; ++r) b.v(r) = t_fma(-bi, LU(r, i), b.v(r));
+  }
+}
+
+// smem path when n >= NLK_SMEM_LU_MIN and the N*N + N slice of a 128-thread
+// block fits in 200 KB (f64: n <= 14; larger n keep the register path)
+template <int N, class T, int MIN_N> struct UseSmemLU {
+  static constexpr bool value =
+      N >= MIN_N && sizeof(T) * (N * N + N) * kSmStride <= 200 * 1024;
+  // GETF2 panels need blocking <= 8 (getrf_single recursion depth 1)
+  static_assert(!value || N <= 17, "shared-memory getrf models one blocking level");
+};
+
+#undef NLK_SMU
+#undef NLK_FD
+}  // namespace nlk

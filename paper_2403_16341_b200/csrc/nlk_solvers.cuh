@@ -15,6 +15,7 @@
 // accepted steps.
 #pragma once
 #include "nlk_problems.cuh"
+#include "nlk_smem_lu.cuh"
 
 namespace nlk {
 
@@ -110,6 +111,8 @@ struct Base {
   T u[N], f[N];
   T p[M > 0 ? M : 1];
   int k, nsteps, nf, njac, nlinsolve;
+  static constexpr int kSmemElems = 0;
+  T* sm;  // this thread's shared-memory slice (stride kSmStride), see kSmemElems
 
   NLK_FD void F(const T* x, T* out) {  // CountedResidual.at (core.py:119-123)
     nf += 1;
@@ -136,6 +139,8 @@ struct Base {
 template <class P, int N, class T, bool LS>
 struct NewtonRaphson : Base<P, N, T> {
   using B = Base<P, N, T>;
+  static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_NR_MIN>::value;
+  static constexpr int kSmemElems = SM ? N * N + N : 0;
   NLK_FD int init(T abstol) { return B::start(abstol); }
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
@@ -147,12 +152,25 @@ struct NewtonRaphson : Base<P, N, T> {
 #pragma unroll
       for (int i = 0; i < N * N; ++i) Jf[i] = J[i];
     }
-    if (!lu_factor<N>(J, piv)) return LINSOLVE_FAILED;
-    B::nlinsolve += 1;
     T du[N];
+    if constexpr (SM) {
+      const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
 #pragma unroll
-    for (int i = 0; i < N; ++i) du[i] = -B::f[i];
-    getrs<N>(J, piv, du);
+      for (int e = 0; e < N * N; ++e) A.v(e) = J[e];
+      if (!sm_lu_factor<N>(A, piv)) return LINSOLVE_FAILED;
+      B::nlinsolve += 1;
+#pragma unroll
+      for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
+      sm_getrs<N>(A, piv, rhs);
+#pragma unroll
+      for (int i = 0; i < N; ++i) du[i] = rhs.v(i);
+    } else {
+      if (!lu_factor<N>(J, piv)) return LINSOLVE_FAILED;
+      B::nlinsolve += 1;
+#pragma unroll
+      for (int i = 0; i < N; ++i) du[i] = -B::f[i];
+      getrs<N>(J, piv, du);
+    }
     T alpha = T(1);
     T un[N], fn[N];
     if constexpr (LS) {
@@ -190,7 +208,9 @@ struct NewtonRaphson : Base<P, N, T> {
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T> {
   using B = Base<P, N, T>;
-  T J[N * N], LU[N * N];
+  static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_TR_MIN>::value;
+  static constexpr int kSmemElems = SM ? N * N + N : 0;
+  T J[N * N], LU[SM ? 1 : N * N];
   int piv[N];
   T radius, radius_max;
   bool cached;
@@ -206,9 +226,18 @@ struct TrustRegion : Base<P, N, T> {
   // dogleg_direction (descent.py:78-106)
   NLK_FD void dogleg(T* out) {
     T newton[N];
+    if constexpr (SM) {
+      const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
 #pragma unroll
-    for (int i = 0; i < N; ++i) newton[i] = -B::f[i];
-    getrs<N>(LU, piv, newton);
+      for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
+      sm_getrs<N>(A, piv, rhs);
+#pragma unroll
+      for (int i = 0; i < N; ++i) newton[i] = rhs.v(i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) newton[i] = -B::f[i];
+      getrs<N>(LU, piv, newton);
+    }
     if (norm2<N>(newton) <= radius) {
 #pragma unroll
       for (int i = 0; i < N; ++i) out[i] = newton[i];
@@ -243,9 +272,16 @@ struct TrustRegion : Base<P, N, T> {
     B::k += 1;
     if (!cached) {
       if (B::jac(J) >= 0) return NONFINITE;
+      if constexpr (SM) {
+        const SMat<N, T> A{B::sm};
 #pragma unroll
-      for (int i = 0; i < N * N; ++i) LU[i] = J[i];
-      if (!lu_factor<N>(LU, piv)) return LINSOLVE_FAILED;
+        for (int e = 0; e < N * N; ++e) A.v(e) = J[e];
+        if (!sm_lu_factor<N>(A, piv)) return LINSOLVE_FAILED;
+      } else {
+#pragma unroll
+        for (int i = 0; i < N * N; ++i) LU[i] = J[i];
+        if (!lu_factor<N>(LU, piv)) return LINSOLVE_FAILED;
+      }
       cached = true;
     }
     B::nlinsolve += 1;
