@@ -383,7 +383,8 @@ struct CoopBase {
 
   NLK_FD void F(const T* x, T* out) {
     nf += 1;
-    P::template f<T, T>(x, p, out);
+    Ctx<T, 0> cx{nullptr, 0};
+    P::template f<T, T>(x, p, out, cx);
   }
   // column `row` of J by a width-1 dual sweep; returns -1 or the reference
   // chunk index that raised NonFiniteValue.  Fills arow (row) and, if
@@ -396,7 +397,8 @@ struct CoopBase {
       xd[i].v = u[i];
       xd[i].d[0] = (i == g.row) ? T(1) : T(0);
     }
-    P::template f<Dual<1, T>, T>(xd, p, out);
+    Ctx<T, 0> cx{nullptr, 0};
+    P::template f<Dual<1, T>, T>(xd, p, out, cx);
     bool vals_ok = true, col_ok = true;
 #pragma unroll
     for (int i = 0; i < N; ++i) {

@@ -12,6 +12,8 @@
 // two paths differently (pairwise vs sequential sums, BLAS vs object matmul),
 // the helpers below branch on the path.
 #pragma once
+#include <type_traits>
+
 #include "nlk_blas.cuh"
 
 namespace nlk {
@@ -78,17 +80,88 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
   }
 }
 
+// ---- transcendental memo ------------------------------------------------------
+// nlkit evaluates the Jacobian's value path with the same libm calls, on the
+// same point, as the residual evaluation that preceded it (F(u) always comes
+// before J(u) in every driver), and each dense_jacobian chunk repeats them
+// again.  Residuals route their memo-able transcendentals through `cx`:
+//   MODE 1 (float path)  evaluates and records each value in order;
+//   MODE 2 (dual path)   replays the recorded values (bit-identical, same
+//                        function of the same input) and forms the partials;
+//   MODE 0               plain evaluation, nothing recorded.
+// Only functions whose float and dual paths call the same libm routine are
+// memoised (np.sin/np.cos/np.arctan/x**3 == math.*; np.exp is SVML, not
+// glibc, so exp is not), and only where both paths feed them the same bits
+// (helical_valley's atan(x1/x0) is not: Dual division multiplies by the
+// reciprocal).  `kMemo` = slots a residual records per evaluation.
+template <class T, int MODE>
+struct Ctx {
+  T* m;
+  int i;
+  template <class S> NLK_FD void sincos(const S& x, S& s, S& c) {
+    if constexpr (MODE == 2 && IsDual<S>::value) {
+      const T sv = m[i], cv = m[i + 1];
+      s.v = sv;
+      c.v = cv;
+#pragma unroll
+      for (int j = 0; j < (int)(sizeof(x.d) / sizeof(x.d[0])); ++j) {
+        s.d[j] = cv * x.d[j];   // Dual.sin (autodiff.py:202-204)
+        c.d[j] = -sv * x.d[j];  // Dual.cos (autodiff.py:206-208)
+      }
+    } else {
+      t_sincos(x, s, c);
+      if constexpr (MODE == 1) { m[i] = value_of(s); m[i + 1] = value_of(c); }
+    }
+    i += 2;
+  }
+  template <class S> NLK_FD S cos(const S& x) {
+    S s, c;
+    sincos(x, s, c);
+    return c;
+  }
+  template <class S> NLK_FD S atan(const S& x) {
+    S r;
+    if constexpr (MODE == 2 && IsDual<S>::value) {  // Dual.arctan (autodiff.py:214-217)
+      const T c = T(1) / (T(1) + x.v * x.v);
+      r.v = m[i];
+#pragma unroll
+      for (int j = 0; j < (int)(sizeof(x.d) / sizeof(x.d[0])); ++j) r.d[j] = c * x.d[j];
+    } else {
+      r = t_atan(x);
+      if constexpr (MODE == 1) m[i] = value_of(r);
+    }
+    i += 1;
+    return r;
+  }
+  template <class S> NLK_FD S pow3(const S& x) {
+    S r;
+    if constexpr (MODE == 2 && IsDual<S>::value) {  // Dual.__pow__(3) (autodiff.py:135-136)
+      const T c = T(3) * t_pow2(x.v);
+      r.v = m[i];
+#pragma unroll
+      for (int j = 0; j < (int)(sizeof(x.d) / sizeof(x.d[0])); ++j) r.d[j] = c * x.d[j];
+    } else {
+      r = t_pow3(x);
+      if constexpr (MODE == 1) m[i] = value_of(r);
+    }
+    i += 1;
+    return r;
+  }
+};
+template <class P, class = void> struct MemoOf { static constexpr int value = 0; };
+template <class P> struct MemoOf<P, std::void_t<decltype(P::kMemo)>> { static constexpr int value = P::kMemo; };
+
 // ---- the 23-member suite (problems.py:36-292) -------------------------------
 struct Rosenbrock {  // 36-40
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = K(1.0) - x[0];
     out[1] = K(10.0) * (x[1] - x[0] * x[0]);
   }
 };
 struct PowellSingular {  // 43-49
   static constexpr int N = 4, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] + K(10.0) * x[1];
     out[1] = K(2.23606797749979) * (x[2] - x[3]);     // math.sqrt(5.0)
     out[2] = t_pow2(x[1] - K(2.0) * x[2]);
@@ -97,14 +170,14 @@ struct PowellSingular {  // 43-49
 };
 struct PowellBadlyScaled {  // 52-56
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = K(1e4) * x[0] * x[1] - K(1.0);
     out[1] = t_exp(-x[0]) + t_exp(-x[1]) - K(1.0001);
   }
 };
 struct Wood {  // 59-67
   static constexpr int N = 4, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = K(-200.0) * x[0] * (x[1] - t_pow2(x[0])) - (K(1.0) - x[0]);
     out[1] = (K(200.0) * (x[1] - t_pow2(x[0])) + K(20.2) * (x[1] - K(1.0)) + K(19.8) * (x[3] - K(1.0)));
     out[2] = K(-180.0) * x[2] * (x[3] - t_pow2(x[2])) - (K(1.0) - x[2]);
@@ -113,7 +186,7 @@ struct Wood {  // 59-67
 };
 struct HelicalValley {  // 70-81
   static constexpr int N = 3, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     const T twopi = K(6.283185307179586);  // 2.0 * math.pi
     if (x[0] > K(0)) {
       S angle = t_atan(x[1] / x[0]) / twopi;
@@ -131,7 +204,7 @@ struct HelicalValley {  // 70-81
 };
 struct Watson {  // 84-109 (n = 2)
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll 1
     for (int i = 1; i < 30; ++i) {
       T ti = T(i) / K(29.0);
@@ -163,7 +236,7 @@ struct Watson {  // 84-109 (n = 2)
 };
 struct Chebyquad {  // 112-129 (n = 2)
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       S t_cur = K(2.0) * x[j] - K(1.0);
@@ -186,7 +259,7 @@ struct Chebyquad {  // 112-129 (n = 2)
 };
 struct BrownAlmostLinear {  // 132-139
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S total = np_sum<N>(x);
 #pragma unroll
     for (int k = 0; k < N - 1; ++k) out[k] = x[k] + total - K(N + 1.0);
@@ -195,7 +268,8 @@ struct BrownAlmostLinear {  // 132-139
 };
 struct DiscreteBoundaryValue {  // 142-151
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  static constexpr int kMemo = N;
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     const T h = K(1.0) / T(N + 1);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -203,20 +277,21 @@ struct DiscreteBoundaryValue {  // 142-151
       S a = K(2.0) * x[k];
       a = (k > 0) ? a - x[k > 0 ? k - 1 : 0] : a - K(0.0);
       a = (k < N - 1) ? a - x[k < N - 1 ? k + 1 : 0] : a - K(0.0);
-      out[k] = a + K(0.5) * h * h * t_pow3(x[k] + tk + K(1.0));
+      out[k] = a + K(0.5) * h * h * cx.pow3(x[k] + tk + K(1.0));
     }
   }
 };
 struct DiscreteIntegral {  // 154-168
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  static constexpr int kMemo = N;
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     const T h = K(1.0) / T(N + 1);
     T t[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) t[j] = T(j + 1) * h;
     S cubes[N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) cubes[j] = t_pow3(x[j] + t[j] + K(1.0));
+    for (int j = 0; j < N; ++j) cubes[j] = cx.pow3(x[j] + t[j] + K(1.0));
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       S s1 = K(0.0) + t[0] * cubes[0];
@@ -237,10 +312,11 @@ struct DiscreteIntegral {  // 154-168
 };
 struct Trigonometric {  // 171-177
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  static constexpr int kMemo = 2 * N;
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S c[N], sn[N];  // np.cos(x) and np.sin(x[k]): one sincos per component
 #pragma unroll
-    for (int k = 0; k < N; ++k) t_sincos(x[k], sn[k], c[k]);
+    for (int k = 0; k < N; ++k) cx.sincos(x[k], sn[k], c[k]);
     S cos_sum = np_sum<N>(c);
 #pragma unroll
     for (int k = 0; k < N; ++k)
@@ -249,7 +325,7 @@ struct Trigonometric {  // 171-177
 };
 struct VariablyDimensioned {  // 180-188
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S w[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) w[k] = T(k + 1) * (x[k] - K(1.0));
@@ -262,7 +338,7 @@ struct VariablyDimensioned {  // 180-188
 template <int NN>
 struct BroydenTridiagonal {  // 191-198 (n-generic)
   static constexpr int N = NN, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       S a = (K(3.0) - K(2.0) * x[k]) * x[k];
@@ -274,7 +350,7 @@ struct BroydenTridiagonal {  // 191-198 (n-generic)
 };
 struct BroydenBanded {  // 201-210
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const int lo = k - 5 > 0 ? k - 5 : 0;
@@ -294,7 +370,7 @@ struct BroydenBanded {  // 201-210
 };
 struct MatrixSqrt2x2 {  // 213-220
   static constexpr int N = 4, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] * x[0] + x[1] * x[2] - K(1e-4);
     out[1] = x[0] * x[1] + x[1] * x[3] - K(1.0);
     out[2] = x[2] * x[0] + x[3] * x[2];
@@ -303,7 +379,7 @@ struct MatrixSqrt2x2 {  // 213-220
 };
 struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
   static constexpr int N = 9, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -326,14 +402,15 @@ struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
 };
 struct DennisSchnabel {  // 233-237
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  static constexpr int kMemo = 1;
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] * x[0] + x[1] * x[1] - K(2.0);
-    out[1] = t_exp(x[0] - K(1.0)) + t_pow3(x[1]) - K(2.0);
+    out[1] = t_exp(x[0] - K(1.0)) + cx.pow3(x[1]) - K(2.0);
   }
 };
 struct ProductExponential {  // 240-251
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     if (x[0] != K(0)) out[0] = x[1] * x[1] * (K(1.0) - t_exp(-x[0] * x[0])) / x[0];
     else out[0] = K(0.0) * x[1];
     if (x[1] != K(0)) out[1] = x[0] * (K(1.0) - t_exp(-x[1] * x[1])) / x[1];
@@ -342,7 +419,7 @@ struct ProductExponential {  // 240-251
 };
 struct CubicRadial {  // 254-260
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S r2 = x[0] * x[0] + x[1] * x[1];
     out[0] = x[0] * r2;
     out[1] = x[1] * r2;
@@ -350,27 +427,28 @@ struct CubicRadial {  // 254-260
 };
 struct DoubleRootScalar {  // 263-266
   static constexpr int N = 1, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] * t_pow2(x[0] - K(5.0));
   }
 };
 struct FreudensteinRoth {  // 269-273
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = K(-13.0) + x[0] + ((K(5.0) - x[1]) * x[1] - K(2.0)) * x[1];
     out[1] = K(-29.0) + x[0] + ((K(1.0) + x[1]) * x[1] - K(14.0)) * x[1];
   }
 };
 struct Boggs {  // 276-280
   static constexpr int N = 2, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  static constexpr int kMemo = 2;
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] * x[0] - x[1] + K(1.0);
-    out[1] = x[0] - t_cos(K(1.5707963267948966) * x[1]);  // (0.5 * math.pi) * x1
+    out[1] = x[0] - cx.cos(K(1.5707963267948966) * x[1]);  // (0.5 * math.pi) * x1
   }
 };
 struct Chandrasekhar {  // 286-292
   static constexpr int N = 10, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     T mu[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) mu[i] = (T(i + 1) - K(0.5)) / T(N);
@@ -400,7 +478,7 @@ struct Chandrasekhar {  // 286-292
 template <int NN>
 struct GeneralizedRosenbrock {  // 363-368
   static constexpr int N = NN, M = 0;
-  template <class S, class T> NLK_FD static void f(const S* x, const T*, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = K(1.0) - x[0];
 #pragma unroll
     for (int i = 1; i < N; ++i) out[i] = K(10.0) * (x[i] - x[i - 1] * x[i - 1]);
@@ -409,7 +487,7 @@ struct GeneralizedRosenbrock {  // 363-368
 template <int NN>
 struct Quadratic {  // 382-383: u * u - theta
   static constexpr int N = NN, M = NN;
-  template <class S, class T> NLK_FD static void f(const S* x, const T* p, S* out) {
+  template <class S, class T, class C> NLK_FD static void f(const S* x, const T* p, S* out, C& cx) {
 #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];
   }

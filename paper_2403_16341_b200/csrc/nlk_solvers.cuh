@@ -61,11 +61,17 @@ template <int N> struct SweepWidth {
   static constexpr int value = N <= 4 ? N : (N < NLK_SWEEP_MAX ? N : NLK_SWEEP_MAX);
 };
 
+// J sinks: register array or shared-memory slice (column-major, e = i + j*N)
+template <class T> NLK_FD void jput(T* J, int e, T v) { J[e] = v; }
+template <int N, class T> NLK_FD void jput(const SMat<N, T>& J, int e, T v) { J.v(e) = v; }
+
 // dense_jacobian (autodiff.py:342-355) into column-major J.  Returns -1 on
 // success, else the index of the reference chunk (8 columns) whose check
 // raised NonFiniteValue — nlkit evaluates chunks up to and including it.
-template <class P, int N, class T, int C0>
-NLK_FD void jac_sweeps(const T* u, const T* p, T* J, bool& vals_ok, int& bad_col) {
+// `memo` holds the transcendental values recorded by the last F(u) (see Ctx
+// in nlk_problems.cuh); every sweep replays them.
+template <class P, int N, class T, int C0, class JS>
+NLK_FD void jac_sweeps(const T* u, const T* p, T* memo, JS J, bool& vals_ok, int& bad_col) {
   if constexpr (C0 < N) {
     constexpr int SW = SweepWidth<N>::value;
     constexpr int W = (N - C0) < SW ? (N - C0) : SW;
@@ -76,7 +82,8 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* J, bool& vals_ok, int& bad_col
 #pragma unroll
       for (int j = 0; j < W; ++j) xd[i].d[j] = (i == C0 + j) ? T(1) : T(0);
     }
-    P::template f<Dual<W, T>, T>(xd, p, out);
+    Ctx<T, (MemoOf<P>::value > 0 ? 2 : 0)> cx{memo, 0};
+    P::template f<Dual<W, T>, T>(xd, p, out, cx);
     if constexpr (C0 == 0) {
 #pragma unroll
       for (int i = 0; i < N; ++i) vals_ok &= isfinite(out[i].v);
@@ -87,19 +94,19 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* J, bool& vals_ok, int& bad_col
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         colok &= isfinite(out[i].d[j]);
-        J[i + (C0 + j) * N] = out[i].d[j];
+        jput(J, i + (C0 + j) * N, out[i].d[j]);
       }
       if (!colok && bad_col > C0 + j) bad_col = C0 + j;
     }
-    jac_sweeps<P, N, T, C0 + W>(u, p, J, vals_ok, bad_col);
+    jac_sweeps<P, N, T, C0 + W>(u, p, memo, J, vals_ok, bad_col);
   }
 }
 
-template <class P, int N, class T>
-NLK_FD int jacobian(const T* u, const T* p, T* J) {
+template <class P, int N, class T, class JS>
+NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
   bool vals_ok = true;
   int bad_col = N;
-  jac_sweeps<P, N, T, 0>(u, p, J, vals_ok, bad_col);
+  jac_sweeps<P, N, T, 0>(u, p, memo, J, vals_ok, bad_col);
   if (!vals_ok) return 0;
   if (bad_col < N) return bad_col / 8;
   return -1;
@@ -114,13 +121,21 @@ struct Base {
   static constexpr int kSmemElems = 0;
   T* sm;  // this thread's shared-memory slice (stride kSmStride), see kSmemElems
 
+  static constexpr int KM = MemoOf<P>::value;
+  T memo[KM > 0 ? KM : 1];  // transcendentals of the last F call
+
   NLK_FD void F(const T* x, T* out) {  // CountedResidual.at (core.py:119-123)
     nf += 1;
-    P::template f<T, T>(x, p, out);
+    Ctx<T, (KM > 0 ? 1 : 0)> cx{memo, 0};
+    P::template f<T, T>(x, p, out, cx);
   }
-  NLK_FD int jac(T* J) {
+  // Precondition (memo): the last F call was at u.  Holds at every call site:
+  // start() evaluates F(u0); Newton accepts u = un right after F(un); the
+  // trust region re-evaluates J only after accepting u = ut right after F(ut).
+  template <class JS>
+  NLK_FD int jac(JS J) {
     njac += 1;
-    int bad = jacobian<P, N, T>(u, p, J);
+    int bad = jacobian<P, N, T>(u, p, memo, J);
     constexpr int chunks = (N + 7) / 8;
     nf += (bad < 0) ? chunks : bad + 1;
     return bad;
@@ -144,19 +159,16 @@ struct NewtonRaphson : Base<P, N, T> {
   NLK_FD int init(T abstol) { return B::start(abstol); }
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
-    T J[N * N];
     int piv[N];
-    if (B::jac(J) >= 0) return NONFINITE;
-    T Jf[LS ? N * N : 1];
-    if constexpr (LS) {
-#pragma unroll
-      for (int i = 0; i < N * N; ++i) Jf[i] = J[i];
-    }
+    T Jf[LS ? N * N : 1];  // J kept for the line search's J @ du
     T du[N];
-    if constexpr (SM) {
+    if constexpr (SM) {  // J streams column by column into the smem slice
       const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
+      if (B::jac(A) >= 0) return NONFINITE;
+      if constexpr (LS) {
 #pragma unroll
-      for (int e = 0; e < N * N; ++e) A.v(e) = J[e];
+        for (int e = 0; e < N * N; ++e) Jf[e] = A.v(e);
+      }
       if (!sm_lu_factor<N>(A, piv)) return LINSOLVE_FAILED;
       B::nlinsolve += 1;
 #pragma unroll
@@ -165,6 +177,12 @@ struct NewtonRaphson : Base<P, N, T> {
 #pragma unroll
       for (int i = 0; i < N; ++i) du[i] = rhs.v(i);
     } else {
+      T J[N * N];
+      if (B::jac(J) >= 0) return NONFINITE;
+      if constexpr (LS) {
+#pragma unroll
+        for (int i = 0; i < N * N; ++i) Jf[i] = J[i];
+      }
       if (!lu_factor<N>(J, piv)) return LINSOLVE_FAILED;
       B::nlinsolve += 1;
 #pragma unroll
