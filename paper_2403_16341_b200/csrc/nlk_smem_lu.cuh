@@ -68,8 +68,10 @@ NLK_SMU
     // 1. earlier interchanges of this panel, applied to column c
 NLK_SMU
     for (int i = 0; i < j; ++i) {
-      const int p = piv[OFF + i];
-      if (p != OFF + i) { T t = A(OFF + i, c); A(OFF + i, c) = A(p, c); A(p, c) = t; }
+      const int p = piv[OFF + i];  // p == row: a no-op swap (branch-free)
+      const T t = A(OFF + i, c);
+      A(OFF + i, c) = A(p, c);
+      A(p, c) = t;
     }
     // 2. rows 1..j-1: b_i -= sdot(L[i, 0:i], b[0:i])
 NLK_SMU
@@ -134,7 +136,7 @@ NLK_SMU
     piv[c] = p;
     // 5. interchange over the finished panel columns and b, then scale
     if (A(p, c) != T(0)) {
-      if (p != c) sm_swap_rows(A, c, p, OFF, c + 1);
+      sm_swap_rows(A, c, p, OFF, c + 1);
       const T bj = A(c, c);
       if (fabs(bj) >= Num<T>::dbl_min) {
         const T rr = T(1) / bj;
@@ -195,7 +197,7 @@ NLK_SMU
       if (is + bk < N) {
 NLK_SMU
         for (int i = is; i < is + bk; ++i)
-          if (piv[i] != i) sm_swap_rows(A, i, piv[i], is + bk, N);
+          sm_swap_rows(A, i, piv[i], is + bk, N);
         sm_trsm(A, is, bk);
         sm_gemm_minus(A, is + bk, N - is - bk, is + bk, N - is - bk, is, bk);
       }
@@ -205,22 +207,28 @@ NLK_SMU
       const int bk = (N - is) < BLK ? (N - is) : BLK;
 NLK_SMU
       for (int i = is + bk; i < N; ++i)
-        if (piv[i] != i) sm_swap_rows(A, i, piv[i], is, is + bk);
+        sm_swap_rows(A, i, piv[i], is, is + bk);
     }
   }
 }
 
-template <int N, class T>
+// JAC_CHECKED: A is a Jacobian that passed dense_jacobian's finiteness
+// checks, so max|A| is finite and the scan below can only reject an all-zero
+// matrix -- which getrf rejects anyway (every pivot is zero), with the same
+// outcome (SingularMatrix -> LINSOLVE_FAILED).  The scan is skipped then.
+template <int N, bool JAC_CHECKED, class T>
 NLK_FD bool sm_lu_factor(const SMat<N, T>& A, int* piv) {
-  T anorm = T(0);
-  bool nan = false;
+  if constexpr (!JAC_CHECKED) {
+    T anorm = T(0);
+    bool nan = false;
 NLK_SMU
-  for (int e = 0; e < N * N; ++e) {
-    const T a = fabs(A.v(e));
-    nan |= (a != a);
-    anorm = a > anorm ? a : anorm;
+    for (int e = 0; e < N * N; ++e) {
+      const T a = fabs(A.v(e));
+      nan |= (a != a);
+      anorm = a > anorm ? a : anorm;
+    }
+    if (nan || anorm == T(0) || !isfinite(anorm)) return false;
   }
-  if (nan || anorm == T(0) || !isfinite(anorm)) return false;
   sm_getrf(A, piv);
   bool zero = false, pnan = false;
 NLK_SMU
@@ -238,7 +246,9 @@ NLK_FD void sm_getrs(const SMat<N, T>& LU, const int* piv, const SMat<N, T>& b) 
 NLK_SMU
   for (int i = 0; i < N; ++i) {
     const int p = piv[i];
-    if (p != i) { T t = b.v(i); b.v(i) = b.v(p); b.v(p) = t; }
+    const T t = b.v(i);
+    b.v(i) = b.v(p);
+    b.v(p) = t;
   }
 NLK_SMU
   for (int i = 0; i < N; ++i) {

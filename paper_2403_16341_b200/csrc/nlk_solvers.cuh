@@ -169,7 +169,7 @@ struct NewtonRaphson : Base<P, N, T> {
 #pragma unroll
         for (int e = 0; e < N * N; ++e) Jf[e] = A.v(e);
       }
-      if (!sm_lu_factor<N>(A, piv)) return LINSOLVE_FAILED;
+      if (!sm_lu_factor<N, true>(A, piv)) return LINSOLVE_FAILED;
       B::nlinsolve += 1;
 #pragma unroll
       for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
@@ -294,7 +294,7 @@ struct TrustRegion : Base<P, N, T> {
         const SMat<N, T> A{B::sm};
 #pragma unroll
         for (int e = 0; e < N * N; ++e) A.v(e) = J[e];
-        if (!sm_lu_factor<N>(A, piv)) return LINSOLVE_FAILED;
+        if (!sm_lu_factor<N, true>(A, piv)) return LINSOLVE_FAILED;
       } else {
 #pragma unroll
         for (int i = 0; i < N * N; ++i) LU[i] = J[i];

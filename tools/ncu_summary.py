@@ -31,8 +31,12 @@ def main(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, vals = rows[0], rows[2]
-    d = dict(zip(hdr, vals))
+    hdr = rows[0]
+    for vals in rows[2:]:
+        summarize(path, dict(zip(hdr, vals)))
+
+
+def summarize(path, d):
     print(f"== {path}  kernel: {d.get('Kernel Name', '?')[:90]}")
     for k, label in KEYS:
         if k in d:
@@ -46,7 +50,6 @@ def main(path):
                 pass
     stalls.sort(reverse=True)
     print("  top stalls (warps per issue):", ", ".join(f"{n} {v:.2f}" for v, n in stalls[:6]))
-
 
 if __name__ == "__main__":
     for p in sys.argv[1:]:
