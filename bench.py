@@ -315,14 +315,19 @@ def run_ours(args, rank, world, local_rank, dist):
                     torch.empty((4, Bj), dtype=torch.int32).pin_memory())
             host.append((h_, ALG_ID[alg_], Bj, hu0, hp, hout))
 
+        e2e_job_s = [0.0] * len(host)
+
         def e2e_step():
-            for h_, a_, Bj, hu0, hp, (uo, ro, rc, cn) in host:
+            for j, (h_, a_, Bj, hu0, hp, (uo, ro, rc, cn)) in enumerate(host):
+                tj = time.perf_counter()
                 _lib.check(L.nlk_solve_batch_host(
                     h_, a_, 0, Bj, hu0.data_ptr(), None if hp is None else hp.data_ptr(), 1e-8,
                     1000, uo.data_ptr(), ro.data_ptr(), rc.data_ptr(), cn[0].data_ptr(),
                     cn[1].data_ptr(), cn[2].data_ptr(), cn[3].data_ptr(), 0, 0))
+                e2e_job_s[j] += time.perf_counter() - tj
 
         e2e_step()  # warm-up (allocations, first-touch)
+        e2e_job_s = [0.0] * len(host)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -337,6 +342,17 @@ def run_ours(args, rank, world, local_rank, dist):
         e2e = {"value": world * per_step_systems * args.e2e_steps / float(te.item()),
                "unit": "systems/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "steps": args.e2e_steps}
+        stats["e2e_per_job_ms"] = dict(zip(kernel_names, [round(1e3 * v / args.e2e_steps, 3)
+                                                          for v in e2e_job_s]))
+
+    # roofline.traffic: DRAM bytes of the dominant kernel from a committed ncu --set full
+    # capture (profiles/ncu_traffic.json), scaled to this run's batch; null if none matches
+    traffic = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get(kernel_names[jdom])
+        if t:
+            traffic = t["dram_bytes"] * (prepared[jdom][5].shape[1] / t["batch"])
 
     result = {
         "metric": METRIC, "value": value, "unit": "systems/s", "n_gpus": world,
@@ -350,7 +366,9 @@ def run_ours(args, rank, world, local_rank, dist):
                    "parallelism": f"shard{world} (independent systems, no collective)"},
         "gpu_launches": len(prepared) * args.steps,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
-                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
+                     "algorithmic_bytes": flops.system_bytes(n, m) * prepared[jdom][5].shape[1],
                      "kernel": kernel_names[jdom], "launch_ms": launch_ms[jdom],
                      "flops_per_launch": F,
                      "peak_source": "nlk_fp64_peak (DFMA chains, measured in this run)",
