@@ -111,6 +111,27 @@ NLK_API int nlk_last_grid(void);
  * bound rather than HBM- or tensor-bound. */
 NLK_API int nlk_fp64_peak(int64_t iters, double* tflops_out, void* stream);
 
+/* Implicit-function-theorem sensitivities at B roots of one parametrised
+ * problem (m > 0), device buffers, asynchronous on `stream`.
+ *   nlk_ift_forward_batch  replaces sensitivity.ift_forward(problem, u_star,
+ *     theta, abstol, full) (sensitivity.py:40-57): S_out = d(u_star)/d(theta),
+ *     [n*m][B] with S[i][j] of system b at (i*m + j)*B + b;
+ *   nlk_ift_adjoint_batch  replaces sensitivity.ift_adjoint(problem, u_star,
+ *     theta, gbar, abstol, full) (sensitivity.py:60-80): grad_out [m][B].
+ * u_star_soa [n][B], theta_soa [m][B], gbar_soa [n][B].  solve_resid_out
+ * ([B], may be NULL) is the `full=True` SensitivityResult.solve_residual.
+ * status_out[b]: 0 ok, 1 not a root (the reference raises ValueError,
+ * sensitivity.py:31-36), 2 SingularMatrix (strict LU, linalg.py:87-105),
+ * 3 NonFiniteValue (dual evaluation); outputs of a failed system are NaN.
+ * dtype must be 0 (f64). */
+NLK_API int nlk_ift_forward_batch(int32_t handle, int32_t dtype, int64_t B, const void* u_star_soa,
+                                  const void* theta_soa, double abstol, void* S_out,
+                                  void* solve_resid_out, int8_t* status_out, void* stream);
+NLK_API int nlk_ift_adjoint_batch(int32_t handle, int32_t dtype, int64_t B, const void* u_star_soa,
+                                  const void* theta_soa, const void* gbar_soa, double abstol,
+                                  void* grad_out, void* solve_resid_out, int8_t* status_out,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

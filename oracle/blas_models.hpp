@@ -19,6 +19,7 @@
 //   getrf     : scipy.linalg.lu_factor (linalg.py:98)
 //   getrs     : scipy.linalg.lu_solve (linalg.py:107-108)
 #pragma once
+#include <vector>
 #include <cmath>
 #include <cstdint>
 
@@ -293,6 +294,30 @@ inline void getrs(int n, const double* LU, const int* piv, double* b) {
   for (int i = n - 1; i >= 0; --i) {
     b[i] = b[i] / LU[i * n + i];
     for (int r = 0; r < i; ++r) b[r] = std::fma(-b[i], LU[r * n + i], b[r]);
+  }
+}
+
+// ---- LAPACK getrs with trans = 'T', one right-hand side ----------------------
+// scipy.linalg.lu_solve(..., trans=1) (linalg.py:110-112, used by
+// sensitivity.ift_adjoint): OpenBLAS getrs_T for one RHS = trsv_TUN
+// (forward: b_i = (b_i - ddot(U[0:i, i], b[0:i])) / U_ii), trsv_TLU
+// (backward: b_i -= ddot(L[i+1:n, i], b[i+1:n])), then the row interchanges
+// in reverse order.  Pinned against scipy in tests/test_oracle_blas.py.
+inline void getrs_t(int n, const double* LU, const int* piv, double* b) {
+  std::vector<double> col(n);
+  for (int i = 0; i < n; ++i) {
+    for (int k = 0; k < i; ++k) col[k] = LU[k * n + i];
+    if (i > 0) b[i] -= ddot(i, col.data(), b);
+    b[i] /= LU[i * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    const int len = n - 1 - i;
+    for (int k = 0; k < len; ++k) col[k] = LU[(i + 1 + k) * n + i];
+    if (len > 0) b[i] -= ddot(len, col.data(), b + i + 1);
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    int p = piv[i];
+    if (p != i) { double t = b[i]; b[i] = b[p]; b[p] = t; }
   }
 }
 

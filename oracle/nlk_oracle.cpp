@@ -591,5 +591,6 @@ void oracle_gemv_A_x(int n, const double* A, const double* x, double* y) { gemv_
 void oracle_gemv_AT_x(int n, const double* A, const double* x, double* y) { gemv_AT_x(n, A, x, y); }
 void oracle_getrf(int n, double* A, int* piv) { getrf(n, A, piv); }
 void oracle_getrs(int n, const double* LU, const int* piv, double* b) { getrs(n, LU, piv, b); }
+void oracle_getrs_t(int n, const double* LU, const int* piv, double* b) { getrs_t(n, LU, piv, b); }
 
 }  // extern "C"

@@ -57,6 +57,7 @@ def lib():
         L.oracle_gemv_AT_x.argtypes = [c_int, dp, dp, dp]
         L.oracle_getrf.argtypes = [c_int, dp, ip]
         L.oracle_getrs.argtypes = [c_int, dp, ip, dp]
+        L.oracle_getrs_t.argtypes = [c_int, dp, ip, dp]
         _lib = L
     return _lib
 
@@ -128,3 +129,67 @@ def sensitivity_mask(problem_id, alg, u0, p=None, abstol=1e-8, maxiters=1000, ba
         r = solve_batch(problem_id, alg, u0, p, abstol, maxiters, nudge=d)
         mask |= (r["retcode"] != base["retcode"]) | (r["nsteps"] != base["nsteps"])
     return mask
+
+
+# ---- IFT sensitivities (sensitivity.py:40-80), restated -----------------------
+def param_jacobian(problem_id, x, theta):
+    """autodiff.param_jacobian (autodiff.py:400-427) for the registry's
+    parametrised family: quadratic f = u*u - θ, whose dual partials are
+    Dual.__rsub__ of the seeds: -1.0 on the diagonal, -0.0 elsewhere."""
+    if problem_id != "quadratic":
+        raise NotImplementedError(problem_id)
+    return -np.eye(len(x), len(theta))
+
+
+def _lu_strict(J):
+    """LuFactorization(J, strict=True) (linalg.py:87-105) on the oracle's
+    getrf model; returns (LU, piv) or None for SingularMatrix."""
+    n = J.shape[0]
+    anorm = float(np.max(np.abs(J)))
+    if anorm == 0.0 or not np.isfinite(anorm):
+        return None
+    LU = np.ascontiguousarray(J.copy())
+    piv = np.zeros(n, np.int32)
+    lib().oracle_getrf(n, LU, piv)
+    tol = np.finfo(float).eps * anorm * n
+    if np.min(np.abs(np.diag(LU))) <= tol:
+        return None
+    return LU, piv
+
+
+def ift(problem_id, u, theta, gbar=None, abstol=1e-8):
+    """One system: returns (status, value, solve_residual) with status
+    0 ok / 1 not a root / 2 SingularMatrix / 3 NonFiniteValue; forward
+    sensitivities when gbar is None, else the adjoint gradient."""
+    u = np.asarray(u, np.float64)
+    theta = np.asarray(theta, np.float64)
+    n, m = len(u), len(theta)
+    r = residual(problem_id, u, theta, n)
+    rmax = float(np.max(np.abs(r)))
+    if not rmax <= 10.0 * abstol:
+        return 1, None, None
+    Ju = jacobian(problem_id, u, theta, n)
+    if Ju is None:
+        return 3, None, None
+    Jt = param_jacobian(problem_id, u, theta)
+    if not np.all(np.isfinite(Jt)):
+        return 3, None, None
+    f = _lu_strict(Ju)
+    if f is None:
+        return 2, None, None
+    LU, piv = f
+    if gbar is None:
+        S = np.empty((n, m))
+        for j in range(m):
+            b = np.ascontiguousarray(-Jt[:, j])
+            lib().oracle_getrs(n, LU, piv, b)
+            S[:, j] = b
+        # Ju @ S: numpy matmul = one FMA chain per element (pinned, test_oracle_ift.py)
+        return 0, S, float(np.max(np.abs(Ju @ S + Jt)))
+    lam = np.ascontiguousarray(np.asarray(gbar, np.float64).copy())
+    lib().oracle_getrs_t(n, LU, piv, lam)
+    g = np.empty(m)
+    lib().oracle_gemv_AT_x(n, np.ascontiguousarray(Jt), lam, g)  # Jt.T @ lam (square Jt)
+    y = np.empty(n)
+    lib().oracle_gemv_AT_x(n, np.ascontiguousarray(Ju), lam, y)
+    return 0, -g, float(np.max(np.abs(y - gbar)))

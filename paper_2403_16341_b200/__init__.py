@@ -13,7 +13,10 @@ it, the first solve does, and fails loudly if it is missing.
 
 from .core import (NonlinearProblem, Problem, RetCode, SolveOptions, SolveResult, Stats,
                    check_convergence, result_to_json)
+from .errors import NlkitError, NonFiniteValue, SingularMatrix
 from .problems import DeviceResidual, get_problem
+from .sensitivity import (SensitivityResult, ift_adjoint, ift_adjoint_batch, ift_forward,
+                          ift_forward_batch)
 from .solvers import (ALGORITHM_PRESETS, AlgorithmSpec, BatchResult, SimpleBroyden,
                       SimpleDFSane, SimpleKlement, SimpleNewtonRaphson, SimpleTrustRegion,
                       list_algorithms, run_algorithm, run_polyalgorithm, run_preset, solve,
@@ -25,7 +28,8 @@ __all__ = [
     "run_polyalgorithm", "list_algorithms", "ALGORITHM_PRESETS", "AlgorithmSpec",
     "SimpleNewtonRaphson", "SimpleTrustRegion", "SimpleBroyden", "SimpleKlement",
     "SimpleDFSane", "solve_batch", "solve_batch_soa", "BatchResult", "DeviceResidual",
-    "get_problem",
+    "get_problem", "ift_forward", "ift_adjoint", "ift_forward_batch", "ift_adjoint_batch",
+    "SensitivityResult", "NlkitError", "NonFiniteValue", "SingularMatrix",
 ]
 
 __version__ = "0.1.0"

@@ -56,6 +56,31 @@ NLK_FD T ddot(const T* x, const T* y) {
   return s;
 }
 template <int N, class T> NLK_FD T norm2(const T* x) { return sqrt(ddot<N, T>(x, x)); }
+// the same model with a length known only after unrolling (trsv dots)
+template <class T>
+NLK_FD T ddot_n(const int n, const T* x, const T* y) {
+  const int n16 = n & ~15;
+  T s = T(0);
+  if (n16 > 0) {
+    T v[4];
+#pragma unroll
+    for (int b = 0; b < n16; b += 16) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        T p0 = x[b + j] * y[b + j];
+        T p1 = x[b + j + 4] * y[b + j + 4];
+        T p2 = x[b + j + 8] * y[b + j + 8];
+        T p3 = x[b + j + 12] * y[b + j + 12];
+        if (b == 0) v[j] = ((p0 + p1) + p2) + p3;
+        else v[j] = (((v[j] + p0) + p1) + p2) + p3;
+      }
+    }
+    s = (v[0] + v[2]) + (v[1] + v[3]);
+  }
+#pragma unroll
+  for (int i = n16; i < n; ++i) s = t_fma(x[i], y[i], s);
+  return s;
+}
 
 // ---- GEMV-N column scheme (getf2 step 3 and `A.T @ x`) ---------------------
 // a(i, k) = A[OFF_R + i + (OFF_C + k) * LDA] (column-major storage).

@@ -11,6 +11,7 @@
 
 #include "nlk_b200.h"
 #include "nlk_registry.cuh"
+#include "nlk_ift.cuh"
 
 namespace {
 
@@ -280,4 +281,57 @@ int nlk_solve_batch_host(int32_t handle, int32_t alg, int32_t dtype, int64_t B, 
   return NLK_OK;
 }
 
+}  // extern "C"
+
+// ---- IFT sensitivities (nlk_ift.cuh) ----------------------------------------
+namespace {
+int ift_common(int32_t handle, int32_t dtype, int64_t B, const void* u, const void* th,
+               double abstol, const void* out, const int8_t* status, bool adjoint,
+               const void* gbar, nlk::IftLauncher* l) {
+  const auto& r = reg();
+  if (handle < 0 || handle >= static_cast<int32_t>(r.all.size()))
+    return fail(NLK_ERR_UNKNOWN_PROBLEM, "invalid problem handle " + std::to_string(handle));
+  if (dtype != NLK_F64) return fail(NLK_ERR_NOT_COMPILED, "sensitivities are compiled for f64 only");
+  if (!(abstol > 0)) return fail(NLK_ERR_BAD_OPTIONS, "abstol must be > 0");
+  if (B < 0) return fail(NLK_ERR_BAD_ARGUMENT, "batch size must be >= 0");
+  const nlk::Entry* e = r.all[handle];
+  if (B > 0 && (!u || !th || !out || !status || (adjoint && !gbar)))
+    return fail(NLK_ERR_BAD_ARGUMENT, "u_star, theta, output and status buffers are required");
+  const nlk::IftTable t = nlk::registry_ift();
+  for (int i = 0; i < t.count; ++i) {
+    if (std::strcmp(t.entries[i].id, e->id) == 0 && t.entries[i].n == e->n) {
+      *l = adjoint ? t.entries[i].adjoint : t.entries[i].forward;
+      return NLK_OK;
+    }
+  }
+  return fail(NLK_ERR_NOT_COMPILED, std::string(e->id) + " n=" + std::to_string(e->n) +
+                                        " has no sensitivity kernel (parametrised problems only)");
+}
+}  // namespace
+
+extern "C" {
+int nlk_ift_forward_batch(int32_t handle, int32_t dtype, int64_t B, const void* u_star_soa,
+                          const void* theta_soa, double abstol, void* S_out, void* solve_resid_out,
+                          int8_t* status_out, void* stream) {
+  nlk::IftLauncher l = nullptr;
+  int rc = ift_common(handle, dtype, B, u_star_soa, theta_soa, abstol, S_out, status_out, false,
+                      nullptr, &l);
+  if (rc != NLK_OK || B == 0) return rc;
+  nlk::IftArgs a{B, u_star_soa, theta_soa, nullptr, abstol, S_out, solve_resid_out, status_out};
+  cudaError_t ce = l(a, static_cast<cudaStream_t>(stream));
+  return ce == cudaSuccess ? NLK_OK : cuda_fail(ce, "ift kernel launch");
+}
+
+int nlk_ift_adjoint_batch(int32_t handle, int32_t dtype, int64_t B, const void* u_star_soa,
+                          const void* theta_soa, const void* gbar_soa, double abstol,
+                          void* grad_out, void* solve_resid_out, int8_t* status_out,
+                          void* stream) {
+  nlk::IftLauncher l = nullptr;
+  int rc = ift_common(handle, dtype, B, u_star_soa, theta_soa, abstol, grad_out, status_out, true,
+                      gbar_soa, &l);
+  if (rc != NLK_OK || B == 0) return rc;
+  nlk::IftArgs a{B, u_star_soa, theta_soa, gbar_soa, abstol, grad_out, solve_resid_out, status_out};
+  cudaError_t ce = l(a, static_cast<cudaStream_t>(stream));
+  return ce == cudaSuccess ? NLK_OK : cuda_fail(ce, "ift kernel launch");
+}
 }  // extern "C"

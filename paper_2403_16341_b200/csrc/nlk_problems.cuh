@@ -491,6 +491,12 @@ struct Quadratic {  // 382-383: u * u - theta
 #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];
   }
+  // residual with float u and dual θ (autodiff.param_jacobian, autodiff.py:400-427):
+  // `u * u - td` = float64 product, then Dual.__rsub__
+  template <class S, class T> NLK_FD static void f_param(const T* x, const S* p, S* out) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];
+  }
 };
 
 #undef K

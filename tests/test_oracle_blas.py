@@ -35,6 +35,9 @@ def test_blas_models_bit_exact(n):
         b = x.copy()
         L.oracle_getrs(n, np.ascontiguousarray(lu), piv.astype(np.int32), b)
         assert np.array_equal(b, scipy.linalg.lu_solve((lu, piv), x))
+        b = y.copy()  # trans=1: sensitivity.ift_adjoint's solve_transpose (linalg.py:110-112)
+        L.oracle_getrs_t(n, np.ascontiguousarray(lu), piv.astype(np.int32), b)
+        assert np.array_equal(b, scipy.linalg.lu_solve((lu, piv), y, trans=1))
 
 
 def test_getrf_singular_and_subnormal_pivots():
