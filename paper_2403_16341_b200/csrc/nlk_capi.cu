@@ -75,8 +75,25 @@ int validate(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const void* 
   return NLK_OK;
 }
 
+// The refill counter is a stream-ordered 8-byte allocation.  Keep the
+// device's default pool from returning memory to the driver at every
+// synchronisation (release threshold 0 by default), or each first launch
+// after a sync pays a page mapping on the GPU timeline.
+void keep_pool_warm() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 int launch(nlk::Launcher l, const nlk::KernelArgs& a0, cudaStream_t s) {
   nlk::KernelArgs a = a0;
+  keep_pool_warm();
   unsigned long long* counter = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(*counter), s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(counter)");

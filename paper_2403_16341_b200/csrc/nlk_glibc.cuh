@@ -13,8 +13,8 @@
 // Verified bit-exact against libm on >10^7 inputs per function
 // (tests/test_glibc_ports.py compiles this header for the host).
 //
-// Not reproduced: |x| >= 105414350 in sin/cos (glibc's Payne-Hanek branred);
-// those fall back to CUDA's sin/cos.
+// sin/cos of |x| >= 105414350 go through a port of glibc's Payne-Hanek
+// __branred.
 #pragma once
 #include <fenv.h>
 #include <math.h>
@@ -51,6 +51,7 @@ NLK_GLIBC_ACCESSOR(exp_tab)
 NLK_GLIBC_ACCESSOR(pow_log_tab)
 NLK_GLIBC_ACCESSOR(sincos_tab)
 NLK_GLIBC_ACCESSOR(atan_tab)
+NLK_GLIBC_ACCESSOR(toverp)
 #undef NLK_GLIBC_ACCESSOR
 #define NLK_PICK(name, i) tab_##name(i)
 
@@ -286,6 +287,75 @@ NLK_HD int reduce_sincos(double x, double* a, double* da) {
   *da = db + e;
   return n;
 }
+// ---- __branred (sysdeps/ieee754/dbl-64/branred.c; no FMA in this build) ------
+// Payne-Hanek reduction of 105414350 <= |x| < 2^1024 by pi/2 with the
+// 24-bit digits of 2/pi (toverp): returns the quadrant, *a + *aa = x mod pi/2.
+// Order of operations from the libm disassembly (SSE2, no contraction).
+NLK_HD void branred_half(double xh, double* b_out, double* bb_out, double* sum_out) {
+  constexpr double kTm24 = 0x1p-24, kBig = 0x1.8p52, kBig1 = 0x1.8p54;
+  int k = static_cast<int>((asu(xh) >> 52) & 2047);
+  k = (k - 450) / 24;
+  if (k < 0) k = 0;
+  double gor = asd(static_cast<uint64_t>(0x63f00000u - static_cast<uint32_t>((k * 24) << 20)) << 32);
+  double r[6];
+  for (int i = 0; i < 6; ++i) {
+    r[i] = xh * asd(NLK_PICK(toverp, k + i)) * gor;
+    gor *= kTm24;
+  }
+  double sum = 0.0, s;
+  for (int i = 0; i < 3; ++i) {
+    s = (r[i] + kBig) - kBig;
+    sum += s;
+    r[i] -= s;
+  }
+  double t = 0.0;
+  for (int i = 0; i < 6; ++i) t += r[5 - i];
+  double bb = (((((r[0] - t) + r[1]) + r[2]) + r[3]) + r[4]) + r[5];
+  s = (t + kBig) - kBig;
+  sum += s;
+  t -= s;
+  const double b = t + bb;
+  bb = (t - b) + bb;
+  s = (sum + kBig1) - kBig1;
+  sum -= s;
+  *b_out = b;
+  *bb_out = bb;
+  *sum_out = sum;
+}
+NLK_HD int branred(double x, double* a, double* aa) {
+  constexpr double kTm600 = 0x1p-600, kSplit = 134217729.0;
+  constexpr double kBrMp1 = 0x1.921fb58p+0, kBrMp2 = -0x1.dde974p-27;
+  x *= kTm600;
+  double t = x * kSplit;
+  const double x1 = t - (t - x);
+  const double x2 = x - x1;
+  double b1, bb1, sum1, b2, bb2, sum2;
+  branred_half(x1, &b1, &bb1, &sum1);
+  branred_half(x2, &b2, &bb2, &sum2);
+  double sum = sum1 + sum2;
+  double b = b1 + b2;
+  double bb = (fabs(b1) > fabs(b2)) ? (b1 - b) + b2 : (b2 - b) + b1;
+  if (b > 0.5) {
+    b -= 1.0;
+    sum += 1.0;
+  } else if (b < -0.5) {
+    b += 1.0;
+    sum -= 1.0;
+  }
+  double s = b + (bb + bb1 + bb2);
+  t = ((b - s) + bb) + (bb1 + bb2);
+  b = s * kSplit;
+  const double t1 = b - (b - s);
+  const double t2 = s - t1;
+  b = s * kHp0;
+  bb = (((t1 * kBrMp1 - b) + t1 * kBrMp2) + t2 * kBrMp1) + (t2 * kBrMp2 + s * kHp1 + t * kHp0);
+  s = b + bb;
+  t = (b - s) + bb;
+  *a = s;
+  *aa = t;
+  return static_cast<int>(sum) & 3;
+}
+
 NLK_HD double sin(double x) {
   const uint32_t k = static_cast<uint32_t>(asu(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e500000u) return x;
@@ -301,7 +371,10 @@ NLK_HD double sin(double x) {
     return (n & 2) ? -r : r;
   }
   if (k >= 0x7ff00000u) return x / x;
-  return ::sin(x);
+  double a, da;
+  const int n = branred(x, &a, &da);
+  const double r = (n & 1) ? do_cos_tab(a, da) : do_sin(a, da);
+  return (n & 2) ? -r : r;
 }
 NLK_HD double cos(double x) {
   const uint32_t k = static_cast<uint32_t>(asu(x) >> 32) & 0x7fffffffu;
@@ -320,7 +393,10 @@ NLK_HD double cos(double x) {
     return (n & 2) ? -r : r;
   }
   if (k >= 0x7ff00000u) return x / x;
-  return ::cos(x);
+  double a, da;
+  const int n = branred(x, &a, &da) + 1;
+  const double r = (n & 1) ? do_cos_tab(a, da) : do_sin(a, da);
+  return (n & 2) ? -r : r;
 }
 
 // sin and cos of the same argument in one evaluation, each bit-identical to
@@ -342,9 +418,9 @@ NLK_HD void sincos(double x, double* s, double* c) {
     *c = do_sin(a, da);
     return;
   }
-  if (k < 0x419921fbu) {  // |x| < 105414350: reduce once, both from (a, da, n)
+  if (k < 0x7ff00000u) {  // reduce once (Cody-Waite below 105414350, else branred)
     double a, da;
-    const int n = reduce_sincos(x, &a, &da);
+    const int n = (k < 0x419921fbu) ? reduce_sincos(x, &a, &da) : branred(x, &a, &da);
     const double vs = do_sin(a, da);
     const double vc = do_cos_tab(a, da);
     const double rs = (n & 1) ? vc : vs;
@@ -353,8 +429,7 @@ NLK_HD void sincos(double x, double* s, double* c) {
     *c = ((n + 1) & 2) ? -rc : rc;
     return;
   }
-  *s = glibc::sin(x);
-  *c = glibc::cos(x);
+  *s = *c = x / x;  // inf / NaN -> NaN (glibc: x / x)
 }
 
 // ---- atan (sysdeps/ieee754/dbl-64/s_atan.c, 2.35+ table version, FMA build) --

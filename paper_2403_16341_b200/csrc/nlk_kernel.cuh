@@ -187,22 +187,29 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
     else return solve_kernel<P, N, T, ALG>;
   }();
   constexpr int per_block_systems = UseCoop<N, ALG>::value ? (kThreads / 32) * CoopShape<N>::SPW : kThreads;
-  int dev = 0, sms = 0, per_sm = 0;
+  // occupancy and the smem attribute are per kernel and device: computed once
+  static thread_local int cached_dev = -1, cached_sms = 0, cached_per_sm = 0;
+  int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
   size_t smem = 0;
-  if constexpr (!UseCoop<N, ALG>::value) {
+  if constexpr (!UseCoop<N, ALG>::value)
     smem = sizeof(T) * kThreads * SolverOf<P, N, T, ALG>::type::kSmemElems;
+  if (dev != cached_dev) {
+    int sms = 0, per_sm = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
     }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    cached_dev = dev;
+    cached_sms = sms;
+    cached_per_sm = per_sm < 1 ? 1 : per_sm;
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
+  const int sms = cached_sms, per_sm = cached_per_sm;
   int64_t want = (a.B + per_block_systems - 1) / per_block_systems;
   int64_t grid = static_cast<int64_t>(per_sm) * sms;
   if (want < grid) grid = want;

@@ -51,7 +51,9 @@ def inputs(kind, n, rng):
     if kind == "exp":
         parts = [u * 20, u * 745, u * 1e-3, rng.uniform(-1, 1, n) * 700]
     elif kind in ("sin", "cos"):
-        parts = [u * 10, u * 3, u * 1e5, u * 1e-3, u * np.exp(rng.uniform(-18, 18, n))]
+        parts = [u * 10, u * 3, u * 1e5, u * 1e-3, u * np.exp(rng.uniform(-18, 18, n)),
+                 u * np.exp(rng.uniform(18.4, 709, n)),  # >= 105414350: __branred
+                 np.round(u * 1e12) * 1.0]
     elif kind == "atan":
         parts = [u, u * 20, u * 0.07, u * np.exp(rng.uniform(-40, 40, n))]
     else:

@@ -38,25 +38,16 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
 
 
-# Known gap: glibc's sin/cos reduce arguments |x| >= 105414350 with the
-# Payne-Hanek __branred, which the device does not reproduce (it falls back to
-# CUDA's sin/cos there).  Only diverging trajectories reach such arguments;
-# systems whose reference iterate ended beyond |u| > 3e7 on the sin/cos
-# problems are reported, not gated.
-TRIG_PROBLEMS = {"test23/trigonometric", "test23/boggs"}
-
-
 def check_against(ref, got, what, problem_id=None):
-    exempt = np.zeros(len(ref["retcode"]), bool)
-    if problem_id in TRIG_PROBLEMS:
-        exempt = np.abs(np.asarray(ref["u"])).max(axis=1) > 3e7
-    same = np.ones(len(exempt), bool)
+    """Every field of every system bit-identical (no exemptions: sin/cos of
+    huge arguments go through the port of glibc's __branred)."""
+    same = np.ones(len(ref["retcode"]), bool)
     for k in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
         same &= got[k] == ref[k]
     same &= (bits(got["u"]) == bits(ref["u"])).all(axis=1)
     same &= bits(got["resid"]) == bits(ref["resid"])
-    bad = np.nonzero(~same & ~exempt)[0]
-    assert len(bad) == 0, f"{what}: {len(bad)} systems differ (e.g. {bad[:8]}); exempt {exempt.sum()}"
+    bad = np.nonzero(~same)[0]
+    assert len(bad) == 0, f"{what}: {len(bad)} systems differ (e.g. {bad[:8]})"
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["case"] for c in CASES])
