@@ -17,7 +17,8 @@ Reported on one JSON line (rank 0):
   value    systems solved/s, inputs resident in HBM, CUDA events on the
            launching stream, barrier + synchronize on both sides;
   e2e      same metric through the C-ABI with HOST buffers
-           (nlk_solve_batch_host: pinned H2D, solve, D2H inside the timing);
+           (nlk_solve_batch_host_async per job on 3 streams: pinned H2D,
+           solve, D2H of every output inside the timing);
   roofline dominant kernel: algorithmic FP64 FLOPs (SURVEY.md §8d,
            paper_2403_16341_b200/flops.py) / its CUDA-event duration, against
            the FP64 FMA peak measured on this GPU by nlk_fp64_peak;
@@ -315,19 +316,22 @@ def run_ours(args, rank, world, local_rank, dist):
                     torch.empty((4, Bj), dtype=torch.int32).pin_memory())
             host.append((h_, ALG_ID[alg_], Bj, hu0, hp, hout))
 
-        e2e_job_s = [0.0] * len(host)
+        # every job enqueued through the asynchronous host-buffer entry point,
+        # round-robin over 3 streams (copies of one job overlap the solves of
+        # others), one synchronisation per step
+        e2e_streams = [torch.cuda.Stream(dev) for _ in range(3)]
 
         def e2e_step():
             for j, (h_, a_, Bj, hu0, hp, (uo, ro, rc, cn)) in enumerate(host):
-                tj = time.perf_counter()
-                _lib.check(L.nlk_solve_batch_host(
+                _lib.check(L.nlk_solve_batch_host_async(
                     h_, a_, 0, Bj, hu0.data_ptr(), None if hp is None else hp.data_ptr(), 1e-8,
                     1000, uo.data_ptr(), ro.data_ptr(), rc.data_ptr(), cn[0].data_ptr(),
-                    cn[1].data_ptr(), cn[2].data_ptr(), cn[3].data_ptr(), 0, 0))
-                e2e_job_s[j] += time.perf_counter() - tj
+                    cn[1].data_ptr(), cn[2].data_ptr(), cn[3].data_ptr(),
+                    e2e_streams[j % 3].cuda_stream))
+            for st_ in e2e_streams:
+                st_.synchronize()
 
         e2e_step()  # warm-up (allocations, first-touch)
-        e2e_job_s = [0.0] * len(host)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -342,8 +346,6 @@ def run_ours(args, rank, world, local_rank, dist):
         e2e = {"value": world * per_step_systems * args.e2e_steps / float(te.item()),
                "unit": "systems/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "steps": args.e2e_steps}
-        stats["e2e_per_job_ms"] = dict(zip(kernel_names, [round(1e3 * v / args.e2e_steps, 3)
-                                                          for v in e2e_job_s]))
 
     # roofline.traffic: DRAM bytes of the dominant kernel from a committed ncu --set full
     # capture (profiles/ncu_traffic.json), scaled to this run's batch; null if none matches

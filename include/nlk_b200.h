@@ -101,6 +101,20 @@ NLK_API int nlk_solve_batch_host(int32_t handle, int32_t alg, int32_t dtype, int
                          int32_t* nf_out, int32_t* njac_out, int32_t* nlinsolve_out,
                          int64_t chunk, int32_t num_streams);
 
+/* Asynchronous host-buffer solve: enqueues on `stream` the stream-ordered
+ * allocation of a device staging area, the host->device copy of u0/p, the
+ * solve, the device->host copy of every output and the release of the
+ * staging area, then returns.  Host buffers must stay valid until the stream
+ * reaches that point (synchronise it, or record an event); with pinned host
+ * memory the copies overlap other work on other streams, so a caller can keep
+ * several batches in flight (e.g. one stream per problem batch).  Same
+ * outputs as nlk_solve_batch_host. */
+NLK_API int nlk_solve_batch_host_async(int32_t handle, int32_t alg, int32_t dtype, int64_t B,
+                         const void* u0_soa, const void* p_soa, double abstol, int32_t maxiters,
+                         void* u_out, void* resid_out, int8_t* retcode_out, int32_t* nsteps_out,
+                         int32_t* nf_out, int32_t* njac_out, int32_t* nlinsolve_out,
+                         void* stream);
+
 /* Number of blocks the last nlk_solve_batch launch on this thread used
  * (diagnostics for the persistent grid). */
 NLK_API int nlk_last_grid(void);

@@ -300,6 +300,65 @@ int nlk_solve_batch_host(int32_t handle, int32_t alg, int32_t dtype, int64_t B, 
 
 }  // extern "C"
 
+extern "C" int nlk_solve_batch_host_async(int32_t handle, int32_t alg, int32_t dtype, int64_t B,
+                                          const void* u0_soa, const void* p_soa, double abstol,
+                                          int32_t maxiters, void* u_out, void* resid_out,
+                                          int8_t* retcode_out, int32_t* nsteps_out,
+                                          int32_t* nf_out, int32_t* njac_out,
+                                          int32_t* nlinsolve_out, void* stream) {
+  nlk::Launcher l = nullptr;
+  const nlk::Entry* e = nullptr;
+  int rc = validate(handle, alg, dtype, B, u0_soa, p_soa, abstol, maxiters, u_out, resid_out,
+                    retcode_out, &l, &e);
+  if (rc != NLK_OK || B == 0) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  keep_pool_warm();
+  const size_t es = dtype == NLK_F64 ? 8 : 4;
+  const int n = e->n, m = e->m;
+  // staging: u0 | p | u_out | resid | counters[4] | retcode
+  const size_t bytes = B * es * (2 * n + m + 1) + B * 4 * 4 + B + 256;
+  char* base = nullptr;
+  cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMallocAsync(staging)");
+  char* du0 = base;
+  char* dp = du0 + B * es * n;
+  char* duo = dp + B * es * m;
+  char* dro = duo + B * es * n;
+  int32_t* dcnt = reinterpret_cast<int32_t*>(dro + B * es);
+  int8_t* drc = reinterpret_cast<int8_t*>(dcnt + 4 * B);
+  ce = cudaMemcpyAsync(du0, u0_soa, B * es * n, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess && m > 0) ce = cudaMemcpyAsync(dp, p_soa, B * es * m, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess) {
+    nlk::KernelArgs a{};
+    a.B = B;
+    a.u0 = du0;
+    a.p = m > 0 ? dp : nullptr;
+    a.abstol = abstol;
+    a.maxiters = maxiters;
+    a.u_out = duo;
+    a.resid_out = dro;
+    a.retcode = drc;
+    a.nsteps = nsteps_out ? dcnt : nullptr;
+    a.nf = nf_out ? dcnt + B : nullptr;
+    a.njac = njac_out ? dcnt + 2 * B : nullptr;
+    a.nlinsolve = nlinsolve_out ? dcnt + 3 * B : nullptr;
+    rc = launch(l, a, st);
+  }
+  if (ce == cudaSuccess && rc == NLK_OK) {
+    ce = cudaMemcpyAsync(u_out, duo, B * es * n, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(resid_out, dro, B * es, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(retcode_out, drc, B, cudaMemcpyDeviceToHost, st);
+    int32_t* outs[4] = {nsteps_out, nf_out, njac_out, nlinsolve_out};
+    for (int k = 0; k < 4 && ce == cudaSuccess; ++k)
+      if (outs[k]) ce = cudaMemcpyAsync(outs[k], dcnt + k * B, B * 4, cudaMemcpyDeviceToHost, st);
+  }
+  cudaError_t fe = cudaFreeAsync(base, st);
+  if (rc != NLK_OK) return rc;
+  if (ce != cudaSuccess) return cuda_fail(ce, "nlk_solve_batch_host_async");
+  if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync(staging)");
+  return NLK_OK;
+}
+
 // ---- IFT sensitivities (nlk_ift.cuh) ----------------------------------------
 namespace {
 int ift_common(int32_t handle, int32_t dtype, int64_t B, const void* u, const void* th,

@@ -125,6 +125,36 @@ def test_host_buffer_path_equals_device_path():
     assert np.array_equal(cnt[0], dev["nsteps"]) and np.array_equal(cnt[1], dev["nf"])
 
 
+def test_async_host_path_equals_device_path():
+    """nlk_solve_batch_host_async: two batches in flight on two streams from
+    pinned buffers, results identical to the device-buffer path."""
+    import ctypes
+    outs = []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    jobs = [W.c2_suite(13, 0, 200_003, 0.1), W.c2_suite(11, 0, 150_001, 0.1)]
+    for j, b in enumerate(jobs):
+        h, n, m = _lib.problem_lookup(b.problem_id, b.u0.shape[1])
+        B = len(b.u0)
+        u0 = torch.from_numpy(np.ascontiguousarray(b.u0.T)).pin_memory()
+        o = (torch.empty((n, B), dtype=torch.float64).pin_memory(),
+             torch.empty(B, dtype=torch.float64).pin_memory(),
+             torch.empty(B, dtype=torch.int8).pin_memory(),
+             torch.empty((4, B), dtype=torch.int32).pin_memory())
+        _lib.check(_lib.lib().nlk_solve_batch_host_async(
+            h, 0, 0, B, u0.data_ptr(), None, 1e-8, 1000, o[0].data_ptr(), o[1].data_ptr(),
+            o[2].data_ptr(), o[3][0].data_ptr(), o[3][1].data_ptr(), o[3][2].data_ptr(),
+            o[3][3].data_ptr(), streams[j].cuda_stream))
+        outs.append((b, u0, o))
+    for st in streams:
+        st.synchronize()
+    for b, _u0, (uo, ro, rc, cn) in outs:
+        dev = gpu_solve(b.problem_id, "newton-raphson", b.u0)
+        assert np.array_equal(bits(uo.numpy().T), bits(dev["u"]))
+        assert np.array_equal(bits(ro.numpy()), bits(dev["resid"]))
+        assert np.array_equal(rc.numpy(), dev["retcode"])
+        assert np.array_equal(cn.numpy()[0], dev["nsteps"]) and np.array_equal(cn.numpy()[3], dev["nlinsolve"])
+
+
 @pytest.mark.parametrize("alg", ["newton-raphson", "trust-region", "klement", "dfsane"])
 def test_fp32_against_fp64(alg):
     """fp32 has no reference; where fp32 and fp64 both succeed, u agrees to
