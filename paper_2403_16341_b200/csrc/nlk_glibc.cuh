@@ -400,36 +400,53 @@ NLK_HD double cos(double x) {
 }
 
 // sin and cos of the same argument in one evaluation, each bit-identical to
-// glibc's separate sin() and cos(): the range split is shared, and where both
-// results reduce to the same table row (|x| < 0.855 and the reduced range)
-// the row is read once and both kernels are formed from it.
+// glibc's separate sin() and cos().
 NLK_HD void sincos(double x, double* s, double* c) {
   const uint32_t k = static_cast<uint32_t>(asu(x) >> 32) & 0x7fffffffu;
-  if (k < 0x3feb6000u) {  // |x| < 0.855469
-    *s = (k < 0x3e500000u) ? x : (fabs(x) < kSmall ? taylor_sin(x, 0.0) : do_sin_tab(x, 0.0));
-    *c = (k < 0x3e400000u) ? 1.0 : do_cos_tab(x, 0.0);
+  if (k >= 0x7ff00000u) {  // inf / NaN -> NaN (glibc: x / x)
+    *s = *c = x / x;
     return;
   }
-  if (k < 0x400368fdu) {  // |x| < 2.426265
+  // Every range needs exactly one evaluation of glibc's sine kernel (do_sin:
+  // Taylor below 0.126, else the table) and one of its cosine kernel
+  // (do_cos), at range-dependent arguments.  Classify and reduce first, then
+  // evaluate each kernel once: lanes of a warp in different ranges share the
+  // table code instead of running it once per range (each result is the
+  // value glibc's separate sin() / cos() above return).
+  double as, das, ac, dac;
+  int mode, n = 0;
+  if (k < 0x3feb6000u) {  // |x| < 0.855469: sin(x), cos(x) directly
+    as = ac = x;
+    das = dac = 0.0;
+    mode = 0;
+  } else if (k < 0x400368fdu) {  // |x| < 2.426265: about pi/2
     const double y = kHp0 - fabs(x);
-    *s = copysign(do_cos_tab(y, kHp1), x);
-    const double a = y + kHp1;
-    const double da = (y - a) + kHp1;
-    *c = do_sin(a, da);
-    return;
-  }
-  if (k < 0x7ff00000u) {  // reduce once (Cody-Waite below 105414350, else branred)
+    ac = y;  // sin(x) = copysign(do_cos(y, hp1), x)
+    dac = kHp1;
+    as = y + kHp1;  // cos(x) = do_sin(a, da)
+    das = (y - as) + kHp1;
+    mode = 1;
+  } else {  // Cody-Waite below 105414350, else Payne-Hanek
     double a, da;
-    const int n = (k < 0x419921fbu) ? reduce_sincos(x, &a, &da) : branred(x, &a, &da);
-    const double vs = do_sin(a, da);
-    const double vc = do_cos_tab(a, da);
+    n = (k < 0x419921fbu) ? reduce_sincos(x, &a, &da) : branred(x, &a, &da);
+    as = ac = a;
+    das = dac = da;
+    mode = 2;
+  }
+  const double vs = (fabs(as) < kSmall) ? taylor_sin(as, das) : do_sin_tab(as, das);
+  const double vc = do_cos_tab(ac, dac);
+  if (mode == 0) {
+    *s = (k < 0x3e500000u) ? x : vs;
+    *c = (k < 0x3e400000u) ? 1.0 : vc;
+  } else if (mode == 1) {
+    *s = copysign(vc, x);
+    *c = vs;
+  } else {
     const double rs = (n & 1) ? vc : vs;
     const double rc = ((n + 1) & 1) ? vc : vs;
     *s = (n & 2) ? -rs : rs;
     *c = ((n + 1) & 2) ? -rc : rc;
-    return;
   }
-  *s = *c = x / x;  // inf / NaN -> NaN (glibc: x / x)
 }
 
 // ---- atan (sysdeps/ieee754/dbl-64/s_atan.c, 2.35+ table version, FMA build) --

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(128) ift_kernel(const IftArgs a) {
     int piv[N];
     if (!(rmax <= T(10) * static_cast<T>(a.abstol))) {
       st = IFT_NOT_A_ROOT;
-    } else if (jacobian<P, N, T>(u, th, memo, Ju) >= 0) {
+    } else if (jacobian<P, N, T, KM>(u, th, memo, Ju) >= 0) {
       st = IFT_NONFINITE;
     } else {
       bool ok = true;

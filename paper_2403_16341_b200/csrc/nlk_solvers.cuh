@@ -70,7 +70,7 @@ template <int N, class T> NLK_FD void jput(const SMat<N, T>& J, int e, T v) { J.
 // raised NonFiniteValue — nlkit evaluates chunks up to and including it.
 // `memo` holds the transcendental values recorded by the last F(u) (see Ctx
 // in nlk_problems.cuh); every sweep replays them.
-template <class P, int N, class T, int C0, class JS>
+template <class P, int N, class T, int KM, int C0, class JS>
 NLK_FD void jac_sweeps(const T* u, const T* p, T* memo, JS J, bool& vals_ok, int& bad_col) {
   if constexpr (C0 < N) {
     constexpr int SW = SweepWidth<N>::value;
@@ -82,7 +82,7 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* memo, JS J, bool& vals_ok, int
 #pragma unroll
       for (int j = 0; j < W; ++j) xd[i].d[j] = (i == C0 + j) ? T(1) : T(0);
     }
-    Ctx<T, (MemoOf<P>::value > 0 ? 2 : 0)> cx{memo, 0};
+    Ctx<T, (KM > 0 ? 2 : 0)> cx{memo, 0};
     P::template f<Dual<W, T>, T>(xd, p, out, cx);
     if constexpr (C0 == 0) {
 #pragma unroll
@@ -98,21 +98,24 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* memo, JS J, bool& vals_ok, int
       }
       if (!colok && bad_col > C0 + j) bad_col = C0 + j;
     }
-    jac_sweeps<P, N, T, C0 + W>(u, p, memo, J, vals_ok, bad_col);
+    jac_sweeps<P, N, T, KM, C0 + W>(u, p, memo, J, vals_ok, bad_col);
   }
 }
 
-template <class P, int N, class T, class JS>
+// KM > 0: memo holds the KM transcendental values of F(u) (replayed)
+template <class P, int N, class T, int KM, class JS>
 NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
   bool vals_ok = true;
   int bad_col = N;
-  jac_sweeps<P, N, T, 0>(u, p, memo, J, vals_ok, bad_col);
+  jac_sweeps<P, N, T, KM, 0>(u, p, memo, J, vals_ok, bad_col);
   if (!vals_ok) return 0;
   if (bad_col < N) return bad_col / 8;
   return -1;
 }
 
-template <class P, int N, class T>
+// MEMO: record F's transcendentals for the next Jacobian (drivers that
+// never form a Jacobian -- quasi-Newton, DFSane -- pass false)
+template <class P, int N, class T, bool MEMO = true>
 struct Base {
   static constexpr int M = P::M;
   T u[N], f[N];
@@ -121,7 +124,7 @@ struct Base {
   static constexpr int kSmemElems = 0;
   T* sm;  // this thread's shared-memory slice (stride kSmStride), see kSmemElems
 
-  static constexpr int KM = MemoOf<P>::value;
+  static constexpr int KM = MEMO ? MemoOf<P>::value : 0;
   T memo[KM > 0 ? KM : 1];  // transcendentals of the last F call
 
   NLK_FD void F(const T* x, T* out) {  // CountedResidual.at (core.py:119-123)
@@ -135,7 +138,7 @@ struct Base {
   template <class JS>
   NLK_FD int jac(JS J) {
     njac += 1;
-    int bad = jacobian<P, N, T>(u, p, memo, J);
+    int bad = jacobian<P, N, T, KM>(u, p, memo, J);
     constexpr int chunks = (N + 7) / 8;
     nf += (bad < 0) ? chunks : bad + 1;
     return bad;
@@ -223,9 +226,12 @@ struct NewtonRaphson : Base<P, N, T> {
 };
 
 // ---- trust region with Powell dogleg -----------------------------------------
+#ifndef NLK_TR_MEMO
+#define NLK_TR_MEMO 1
+#endif
 template <class P, int N, class T>
-struct TrustRegion : Base<P, N, T> {
-  using B = Base<P, N, T>;
+struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
+  using B = Base<P, N, T, NLK_TR_MEMO>;
   static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_TR_MIN>::value;
   static constexpr int kSmemElems = SM ? N * N + N : 0;
   T J[N * N], LU[SM ? 1 : N * N];
@@ -349,8 +355,8 @@ struct TrustRegion : Base<P, N, T> {
 
 // ---- quasi-Newton: dense inverse Broyden / diagonal Klement ------------------
 template <class P, int N, class T, bool DIAG>
-struct QuasiNewton : Base<P, N, T> {
-  using B = Base<P, N, T>;
+struct QuasiNewton : Base<P, N, T, false> {
+  using B = Base<P, N, T, false>;
   T H[DIAG ? N : N * N];  // inverse Jacobian (column-major) or Jacobian diagonal
   int reinits, since;
   // stalling window (Klement): min of hist[:-3] and the last three entries
@@ -463,8 +469,8 @@ struct QuasiNewton : Base<P, N, T> {
 
 // ---- DFSane (builder-authored) ------------------------------
 template <class P, int N, class T>
-struct DFSane : Base<P, N, T> {
-  using B = Base<P, N, T>;
+struct DFSane : Base<P, N, T, false> {
+  using B = Base<P, N, T, false>;
   static constexpr int MEM = 10;
   T fnorm, f0, sigma;
   T hist[MEM];
