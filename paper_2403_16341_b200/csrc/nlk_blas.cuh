@@ -120,16 +120,19 @@ NLK_FD void gemv_n_scheme(const int M, const int NCOL, F a, const T* x, T* y) {
 }
 
 // y = A.T @ x, A column-major N x N (A[i + j*N] = A_ij)
-template <int N, class T>
-NLK_FD void gemv_AT_x(const T* A, const T* x, T* y) {
+// A is a register array (T*) or a shared-memory slice (SMat): mat_at(A, e)
+template <class T> NLK_FD T mat_at(const T* A, int e) { return A[e]; }
+
+template <int N, class AM, class T>
+NLK_FD void gemv_AT_x(AM A, const T* x, T* y) {
 #pragma unroll
   for (int i = 0; i < N; ++i) y[i] = T(0);
-  gemv_n_scheme<false>(N, N, [&](int i, int k) { return A[k + i * N]; }, x, y);
+  gemv_n_scheme<false>(N, N, [&](int i, int k) { return mat_at(A, k + i * N); }, x, y);
 }
 
 // y = A @ x (dgemv_t: 4x4 / 4x2 / 4x1 kernels + column tail), A col-major
-template <int N, class T>
-NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
+template <int N, class AM, class T>
+NLK_FD T gemv_t_row(int row, AM A, const T* x) {
   constexpr int N4 = N & ~3;
   T s = T(0);
   if constexpr (N4 > 0) {
@@ -138,14 +141,14 @@ NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
 #pragma unroll
       for (int k = 0; k < N4; k += 4)
 #pragma unroll
-        for (int l = 0; l < 4; ++l) v[l] = t_fma(A[row + (k + l) * N], x[k + l], v[l]);
+        for (int l = 0; l < 4; ++l) v[l] = t_fma(mat_at(A, row + (k + l) * N), x[k + l], v[l]);
       s = (v[0] + v[2]) + (v[1] + v[3]);
     } else if ((N & 2) && row < N4 + 2) {
       T v0 = T(0), v1 = T(0);
 #pragma unroll
       for (int k = 0; k < N4; k += 2) {
-        v0 = v0 + A[row + k * N] * x[k];
-        v1 = v1 + A[row + (k + 1) * N] * x[k + 1];
+        v0 = v0 + mat_at(A, row + k * N) * x[k];
+        v1 = v1 + mat_at(A, row + (k + 1) * N) * x[k + 1];
       }
       s = v0 + v1;
     } else {
@@ -153,7 +156,7 @@ NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
 #pragma unroll
       for (int k = 0; k < N4; k += 4)
 #pragma unroll
-        for (int l = 0; l < 4; ++l) v[l] = v[l] + A[row + (k + l) * N] * x[k + l];
+        for (int l = 0; l < 4; ++l) v[l] = v[l] + mat_at(A, row + (k + l) * N) * x[k + l];
       s = (v[0] + v[2]) + (v[1] + v[3]);
     }
   }
@@ -161,16 +164,16 @@ NLK_FD T gemv_t_row(int row, const T* A, const T* x) {
   if constexpr (R == 0) {
     return s;
   } else if constexpr (R == 1) {
-    return t_fma(A[row + N4 * N], x[N4], s);
+    return t_fma(mat_at(A, row + N4 * N), x[N4], s);
   } else {
-    T t = t_fma(A[row + N4 * N], x[N4], A[row + (N4 + 1) * N] * x[N4 + 1]);
-    if constexpr (R == 3) t = t_fma(A[row + (N4 + 2) * N], x[N4 + 2], t);
+    T t = t_fma(mat_at(A, row + N4 * N), x[N4], mat_at(A, row + (N4 + 1) * N) * x[N4 + 1]);
+    if constexpr (R == 3) t = t_fma(mat_at(A, row + (N4 + 2) * N), x[N4 + 2], t);
     if constexpr (N4 > 0) return s + t;
     else return t;
   }
 }
-template <int N, class T>
-NLK_FD void gemv_A_x(const T* A, const T* x, T* y) {
+template <int N, class AM, class T>
+NLK_FD void gemv_A_x(AM A, const T* x, T* y) {
 #pragma unroll
   for (int i = 0; i < N; ++i) y[i] = gemv_t_row<N>(i, A, x);
 }

@@ -48,6 +48,8 @@ struct SMat {
   NLK_FD T& v(int i) const { return base[i * kSmStride]; }  // as a vector
 };
 
+template <int N, class T> NLK_FD T mat_at(const SMat<N, T>& A, int e) { return A.v(e); }
+
 template <int N, class T>
 NLK_FD void sm_swap_rows(const SMat<N, T>& A, int r1, int r2, int c0, int c1) {
 NLK_SMU

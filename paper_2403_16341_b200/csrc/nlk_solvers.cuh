@@ -229,12 +229,22 @@ struct NewtonRaphson : Base<P, N, T> {
 #ifndef NLK_TR_MEMO
 #define NLK_TR_MEMO 1
 #endif
+#ifndef NLK_TR_JSMEM
+#define NLK_TR_JSMEM 0
+#endif
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
   using B = Base<P, N, T, NLK_TR_MEMO>;
   static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_TR_MIN>::value;
-  static constexpr int kSmemElems = SM ? N * N + N : 0;
-  T J[N * N], LU[SM ? 1 : N * N];
+  // JSM: J also in shared memory (after LU and rhs) instead of registers
+  static constexpr bool JSM =
+      SM && NLK_TR_JSMEM && sizeof(T) * (2 * N * N + N) * kSmStride <= 227 * 1024;
+  static constexpr int kSmemElems = SM ? (JSM ? 2 * N * N + N : N * N + N) : 0;
+  T J[JSM ? 1 : N * N], LU[SM ? 1 : N * N];
+  NLK_FD auto jmat() {
+    if constexpr (JSM) return SMat<N, T>{B::sm + (N * N + N) * kSmStride};
+    else return static_cast<T*>(J);
+  }
   int piv[N];
   T radius, radius_max;
   bool cached;
@@ -268,8 +278,8 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
       return;
     }
     T g[N], Jg[N], cauchy[N];
-    gemv_AT_x<N>(J, B::f, g);
-    gemv_A_x<N>(J, g, Jg);
+    gemv_AT_x<N>(jmat(), B::f, g);
+    gemv_A_x<N>(jmat(), g, Jg);
     T gg = ddot<N>(g, g);
     T jj = ddot<N>(Jg, Jg);
     T t_star = gg / ((Num<T>::tiny > jj) ? Num<T>::tiny : jj);
@@ -295,11 +305,11 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
     if (!cached) {
-      if (B::jac(J) >= 0) return NONFINITE;
+      if (B::jac(jmat()) >= 0) return NONFINITE;
       if constexpr (SM) {
         const SMat<N, T> A{B::sm};
 #pragma unroll
-        for (int e = 0; e < N * N; ++e) A.v(e) = J[e];
+        for (int e = 0; e < N * N; ++e) A.v(e) = mat_at(jmat(), e);
         if (!sm_lu_factor<N, true>(A, piv)) return LINSOLVE_FAILED;
       } else {
 #pragma unroll
@@ -319,7 +329,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
     T rho;
     if (all_finite<N>(ft)) {  // tr_ratio (globalize.py:121-134)
       T Jdu[N], model[N];
-      gemv_A_x<N>(J, du, Jdu);
+      gemv_A_x<N>(jmat(), du, Jdu);
 #pragma unroll
       for (int i = 0; i < N; ++i) model[i] = B::f[i] + Jdu[i];
       T ff = ddot<N>(B::f, B::f);
