@@ -13,6 +13,7 @@
 // refill together claim consecutive indices, so loads/stores coalesce.
 #pragma once
 #include <stdint.h>
+#include <cstdlib>
 
 #include "nlk_coop.cuh"
 
@@ -202,6 +203,15 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
+    }
+    // experiment knob: NLK_CARVEOUT=<percent> caps the shared-memory carve-out
+    // of the smem-LU kernels (fewer blocks per SM, more L1 for spills)
+    if (smem > 0) {
+      static const char* co = std::getenv("NLK_CARVEOUT");
+      if (co) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(co));
+        if (e != cudaSuccess) return e;
+      }
     }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     if (e != cudaSuccess) return e;

@@ -137,7 +137,7 @@ NLK_SMU
     }
     piv[c] = p;
     // 5. interchange over the finished panel columns and b, then scale
-    if (A(p, c) != T(0)) {
+    if (best != T(0)) {  // == (A(p, c) != 0): best is |A(p, c)| (NaN included)
       sm_swap_rows(A, c, p, OFF, c + 1);
       const T bj = A(c, c);
       if (fabs(bj) >= Num<T>::dbl_min) {
