@@ -8,6 +8,7 @@
 #pragma once
 #include <cmath>
 
+#include "npatan.hpp"
 #include "npexp.hpp"
 
 namespace oracle {
@@ -151,14 +152,14 @@ inline Dual np_arctan(const Dual& a) {
 }
 
 // Float-path counterparts: numpy float64 scalar / array ufuncs.  numpy's
-// float64 sin/cos/arctan equal glibc's; numpy's exp is Intel SVML on the
-// reference host (npexp.hpp), not glibc.
+// float64 sin/cos equal glibc's; numpy's exp and arctan are Intel SVML on the
+// reference host (npexp.hpp, npatan.hpp), not glibc.
 inline double pow2(double x) { return libm_pow(x, 2.0); }
 inline double pow3(double x) { return libm_pow(x, 3.0); }
 inline double np_exp(double x) { return svml_exp(x); }
 inline double np_sqrt(double x) { return std::sqrt(x); }
 inline double np_sin(double x) { return libm_sin(x); }
 inline double np_cos(double x) { return libm_cos(x); }
-inline double np_arctan(double x) { return libm_atan(x); }
+inline double np_arctan(double x) { return svml_atan(x); }
 
 }  // namespace oracle

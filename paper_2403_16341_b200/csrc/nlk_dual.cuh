@@ -42,8 +42,9 @@ template <int W, class T> struct ScalarOf<Dual<W, T>> { using type = T; };
 
 // ---- elementary functions --------------------------------------------------------
 // fp64: the reference host's own algorithms (nlk_glibc.cuh): glibc for
-// CPython's math module, numpy's sin/cos/arctan and `x ** n`; Intel SVML for
-// numpy's float64 exp (np.exp on the float path, math.exp on the dual path).
+// CPython's math module, numpy's sin/cos and `x ** n`; Intel SVML for numpy's
+// float64 exp and arctan (np.exp / np.arctan on the float path; the dual path
+// calls math.exp / math.atan).
 // fp32: CUDA's single-precision functions (no reference exists for fp32).
 // Out of line: a residual like test23/trigonometric makes ~60 of these calls
 // per iteration, and inlining each body blew the kernel up to ~25k
@@ -63,7 +64,8 @@ NLK_TRANS_ATTR double nlk_sin(double x) { return glibc::sin(x); }
 NLK_TRANS_ATTR float nlk_sin(float x) { return sinf(x); }
 NLK_TRANS_ATTR double nlk_cos(double x) { return glibc::cos(x); }
 NLK_TRANS_ATTR float nlk_cos(float x) { return cosf(x); }
-NLK_TRANS_ATTR double nlk_atan(double x) { return glibc::atan(x); }
+NLK_TRANS_ATTR double nlk_atan(double x) { return glibc::atan(x); }      // math.atan (Dual path)
+NLK_TRANS_ATTR double nlk_np_atan(double x) { return svml::atan(x); }  // np.arctan on float64
 NLK_TRANS_ATTR double nlk_pow2(double x) { return glibc::pow_int<2>(x); }
 NLK_TRANS_ATTR void nlk_sincos(double x, double* s, double* c) { glibc::sincos(x, s, c); }
 NLK_TRANS_ATTR void nlk_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
@@ -77,8 +79,10 @@ __device__ __forceinline__ double t_sin(double x) { return nlk_sin(x); }
 __device__ __forceinline__ float t_sin(float x) { return nlk_sin(x); }
 __device__ __forceinline__ double t_cos(double x) { return nlk_cos(x); }
 __device__ __forceinline__ float t_cos(float x) { return nlk_cos(x); }
-__device__ __forceinline__ double t_atan(double x) { return nlk_atan(x); }
+__device__ __forceinline__ double t_atan(double x) { return nlk_np_atan(x); }
 __device__ __forceinline__ float t_atan(float x) { return nlk_atan(x); }
+__device__ __forceinline__ double t_atan_math(double x) { return nlk_atan(x); }
+__device__ __forceinline__ float t_atan_math(float x) { return nlk_atan(x); }
 __device__ __forceinline__ double t_sqrt(double x) { return sqrt(x); }
 __device__ __forceinline__ float t_sqrt(float x) { return sqrtf(x); }
 // Python `x ** 2` / `x ** 3` (numpy float64 scalars and CPython floats) call
@@ -207,7 +211,7 @@ NLK_D Dual<W, T> t_cos(const Dual<W, T>& a) {
 }
 NLK_D Dual<W, T> t_atan(const Dual<W, T>& a) {
   T c = T(1) / (T(1) + a.v * a.v);
-  Dual<W, T> r; r.v = t_atan(a.v);
+  Dual<W, T> r; r.v = t_atan_math(a.v);  // Dual.arctan calls math.atan (autodiff.py:214-217)
 #pragma unroll
   for (int i = 0; i < W; ++i) r.d[i] = c * a.d[i];
   return r;

@@ -598,5 +598,117 @@ NLK_HD double exp(double x) {
   // scalef(y, n): y * 2^floor(n), exact for the non-rare range
   return ldexp(y, static_cast<int>(floor(n)));
 }
+
+// ---- np.arctan on float64 = Intel SVML __svml_atan8_ha (numpy 2.3, AVX512_SKX)
+// Transcribed lane-wise from the binary (tables from
+// __svml_datan_ha_data_internal_avx512).  Differs from glibc's atan in ~0.17 %
+// of inputs, which is why the float path (np.arctan) and the dual path
+// (Dual.arctan -> math.atan = glibc) call different functions.
+#define NLK_SVML_ATAN_HI {0x0.0p+0, 0x1.f5b75f92c80ddp-3, 0x1.dac670561bb4fp-2, \
+  0x1.4978fa3269ee1p-1, 0x1.921fb54442d18p-1, 0x1.cac7c57846f9ep-1, 0x1.f730bd281f69bp-1, \
+  0x1.0d38f2c5ba09fp+0, 0x1.1b6e192ebbe44p+0, 0x1.270ef55a53a25p+0, 0x1.30b6d796a4da8p+0, \
+  0x1.38d6a6ce13353p+0, 0x1.3fc176b7a8560p+0, 0x1.45b54837351a0p+0, 0x1.4ae10fc6589a5p+0, \
+  0x1.4f68dea672617p+0, 0x1.5368c951e9cfdp+0, 0x1.56f6f33a3e6a7p+0, 0x1.5a25052114e60p+0, \
+  0x1.5d013c41adabdp+0, 0x1.5f97315254857p+0, 0x1.61f06c6a92b89p+0, 0x1.6414d44094c7cp+0, \
+  0x1.660b02c736a06p+0, 0x1.67d8863bc99bdp+0, 0x1.698213a9d5053p+0, 0x1.6b0bae830c070p+0, \
+  0x1.6c78c7edeb195p+0, 0x1.6dcc57bb565fdp+0, 0x1.6f08f07435fecp+0, 0x1.7030cf9403197p+0, \
+  0x1.7145eac2088a4p+0}
+#define NLK_SVML_ATAN_LO {0x0.0p+0, 0x1.8ab6e3cf7afbdp-57, 0x1.a2b7f222f65e2p-56, \
+  0x1.2419a87f2a458p-56, 0x1.1a62633145c07p-55, 0x1.0dae13ad18a6bp-55, 0x1.007887af0cbbdp-56, \
+  -0x1.bd0dc231bfd70p-54, 0x1.b1b466a88828ep-54, -0x1.a66b1af5f84fbp-54, 0x1.6254cb03bb199p-54, \
+  -0x1.12c77e8a80f5cp-55, -0x1.441a3bd3f1084p-59, 0x1.9e4a72eedacc4p-56, -0x1.3b03e8a27f555p-54, \
+  0x1.934f9f2b0020ep-54, -0x1.96f47948a99f1p-54, -0x1.df6edd6f1ec3bp-56, 0x1.8c2d0c89de218p-56, \
+  0x1.f82bba194dd5dp-54, -0x1.31151a43b51cap-55, -0x1.487d50bceb1a5p-55, -0x1.c5f60a65c7397p-54, \
+  -0x1.acb6afb332a0fp-56, -0x1.9b7bd2e1e8c9cp-54, -0x1.b9839085189e3p-54, -0x1.7d1ab82ffb70bp-54, \
+  0x1.9239ad620ffe2p-54, -0x1.29c86447928e7p-54, -0x1.957a7170df016p-55, -0x1.cbe1896221608p-56, \
+  -0x1.fda5797b32a0bp-54}
+#define NLK_RCP14_TABLE static const uint16_t h_rcp14[65536]
+#include "nlk_rcp14_table.inc"
+#undef NLK_RCP14_TABLE
+static const double h_atan_hi[32] = NLK_SVML_ATAN_HI;
+static const double h_atan_lo[32] = NLK_SVML_ATAN_LO;
+#if defined(__CUDACC__)
+#define NLK_RCP14_TABLE static __device__ const uint16_t d_rcp14[65536]
+#include "nlk_rcp14_table.inc"
+#undef NLK_RCP14_TABLE
+static __device__ const double d_atan_hi[32] = NLK_SVML_ATAN_HI;
+static __device__ const double d_atan_lo[32] = NLK_SVML_ATAN_LO;
+#endif
+NLK_HD double atan_hi(int j) {
+#if defined(__CUDA_ARCH__)
+  return d_atan_hi[j];
+#else
+  return h_atan_hi[j];
+#endif
+}
+NLK_HD double atan_lo(int j) {
+#if defined(__CUDA_ARCH__)
+  return d_atan_lo[j];
+#else
+  return h_atan_lo[j];
+#endif
+}
+// VRCP14PD for a positive normal input (tools/extract_rcp14.c)
+NLK_HD double rcp14(double d) {
+  const uint64_t u = glibc::asu(d);
+  const uint32_t e = static_cast<uint32_t>(u >> 52) & 0x7ffu;
+  const uint32_t m16 = static_cast<uint32_t>(u >> 36) & 0xffffu;
+#if defined(__CUDA_ARCH__)
+  const uint64_t t = d_rcp14[m16];
+#else
+  const uint64_t t = h_rcp14[m16];
+#endif
+  const uint64_t oe = (m16 == 0 ? 2046u : 2045u) - e;
+  return glibc::asd((oe << 52) | (t << 36));
+}
+// x86 MINPD: (a < b) ? a : b, the second operand on NaN
+NLK_HD double minpd(double a, double b) { return a < b ? a : b; }
+
+NLK_HD double atan(double x) {
+  using glibc::dfma;
+  constexpr double kS = 0x1.8p50, kS4 = 0x1.8000000000010p50, kBig = 0x1p128;
+  const double ax = fabs(x);
+  const bool k1 = ax < 7.875;  // table range; else atan(x) = pi/2 - atan(1/x)
+  // reduced argument: vreducepd(ax, 0x28) = ax - RNE(4 ax) / 4 (exact)
+  const double sh = ax + kS;
+  const double b = sh - kS;  // RNE(4 ax) / 4
+  const double t = k1 ? ax - b : -1.0;
+  const int idx = static_cast<int>(glibc::asu(sh) & 15);
+  const bool k2 = sh >= kS4;  // table row 16.. (b >= 4)
+  const double den = k1 ? dfma(b, ax, 1.0) : minpd(kBig, ax);
+  const double r0 = rcp14(den);
+  const double dm1 = den - 1.0;
+  const double dlo = dfma(b, ax, -dm1);
+  const double ahi = k2 ? atan_hi(16 + idx) : atan_hi(idx);
+  const double e = dfma(-r0, den, 1.0);
+  const double e2 = e * e;
+  double r = dfma(e, r0, r0);
+  const double alo = k2 ? atan_lo(16 + idx) : atan_lo(idx);
+  r = dfma(e2, r, r);
+  const double q = r * t;
+  const double dr = dlo * r;
+  double c = dfma(-r, den, 1.0);
+  const double qe = dfma(r, t, -q);
+  c = dfma(q, c, qe);
+  const double q2 = q * q;
+  if (k1) c = dfma(-dr, q, c);
+  const double hi = k1 ? ahi : 0x1.921fb54442d18p+0;
+  const double lo = k1 ? alo : 0x1.1a62633145c07p-54;
+  const double q4 = q2 * q2;
+  const double q3 = q2 * q;
+  double p1 = dfma(0x1.2e9b9f5c4fe97p-4, q2, -0x1.74257c46790ccp-4);
+  const double p2 = dfma(0x1.c71bfeff916a0p-4, q2, -0x1.249248eef04dap-3);
+  const double cl = c + lo;
+  const double s = hi + q;
+  p1 = dfma(q4, p1, p2);
+  const double sh2 = s - hi;
+  const double p3 = dfma(0x1.999999998741ep-3, q2, -0x1.555555555554dp-2);
+  const double tail = q - sh2;
+  p1 = dfma(q4, p1, p3);
+  const double low = cl + tail;
+  p1 = dfma(q3, p1, low);
+  const double res = p1 + s;
+  return glibc::asd(glibc::asu(res) ^ (glibc::asu(x) & 0x8000000000000000ull));
+}
 }  // namespace svml
 }  // namespace nlk

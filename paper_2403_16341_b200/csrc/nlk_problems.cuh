@@ -90,10 +90,9 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
 //                        function of the same input) and forms the partials;
 //   MODE 0               plain evaluation, nothing recorded.
 // Only functions whose float and dual paths call the same libm routine are
-// memoised (np.sin/np.cos/np.arctan/x**3 == math.*; np.exp is SVML, not
-// glibc, so exp is not), and only where both paths feed them the same bits
-// (helical_valley's atan(x1/x0) is not: Dual division multiplies by the
-// reciprocal).  `kMemo` = slots a residual records per evaluation.
+// memoised (np.sin/np.cos/x**3 == math.*; np.exp and np.arctan are SVML on
+// float64, not glibc, so exp and atan are not), and only where both paths
+// feed them the same bits.  `kMemo` = slots a residual records per evaluation.
 template <class T, int MODE>
 struct Ctx {
   T* m;
@@ -118,20 +117,6 @@ struct Ctx {
     S s, c;
     sincos(x, s, c);
     return c;
-  }
-  template <class S> NLK_FD S atan(const S& x) {
-    S r;
-    if constexpr (MODE == 2 && IsDual<S>::value) {  // Dual.arctan (autodiff.py:214-217)
-      const T c = T(1) / (T(1) + x.v * x.v);
-      r.v = m[i];
-#pragma unroll
-      for (int j = 0; j < (int)(sizeof(x.d) / sizeof(x.d[0])); ++j) r.d[j] = c * x.d[j];
-    } else {
-      r = t_atan(x);
-      if constexpr (MODE == 1) m[i] = value_of(r);
-    }
-    i += 1;
-    return r;
   }
   template <class S> NLK_FD S pow3(const S& x) {
     S r;

@@ -187,7 +187,10 @@ def solve_batch_soa(handle, alg, u0_soa, p_soa, abstol=1e-8, maxiters=1000, out=
 def _as_device(x, dtype, device):
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=dtype)
-    return torch.as_tensor(np.asarray(x), dtype=dtype, device=device)
+    a = np.asarray(x)
+    if not a.flags.writeable:  # e.g. np.broadcast_to views: torch wants writable memory
+        a = np.array(a)
+    return torch.as_tensor(a, dtype=dtype, device=device)
 
 
 def solve_batch(problem, u0, p=None, algorithm="newton-raphson", options=None,

@@ -1,0 +1,68 @@
+"""Edge cases on the GPU, through the C ABI:
+  * the reference's outcomes on non-finite / extreme starts, abstol 1e300 and
+    1e-300, maxiters 1, for every algorithm (tests/golden/edges.npz) — every
+    field bit-identical;
+  * empty batches and ragged batch sizes (not multiples of a warp or block),
+    checked against the oracle."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2403_16341_b200 import _lib, solvers, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+CASES = json.load(open(os.path.join(HERE, "edges.json")))
+GOLD = np.load(os.path.join(HERE, "edges.npz"))
+
+
+def _same(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return ((a.view(np.int64) == b.view(np.int64)) | (np.isnan(a) & np.isnan(b))).all()
+
+
+def _solve(pid, alg, u0, p, abstol, maxiters):
+    r = solvers.solve_batch(pid, u0, p, alg, solvers.SolveOptions(abstol, maxiters),
+                            n=u0.shape[1])
+    return r.to_numpy()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["case"] for c in CASES])
+def test_edge_case_matches_reference(case):
+    k = case["case"]
+    g = {x: GOLD[f"{k}/{x}"] for x in ("u0", "p", "u", "resid", "retcode", "nsteps", "nf",
+                                        "njac", "nlinsolve")}
+    p = g["p"] if g["p"].shape[1] else None
+    got = _solve(case["problem_id"], case["alg"], g["u0"], p, case["abstol"], case["maxiters"])
+    for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        assert np.array_equal(got[f], g[f]), f
+    assert _same(got["u"], g["u"]) and _same(got["resid"], g["resid"])
+
+
+def test_empty_batch():
+    h, n, m = _lib.problem_lookup("test23/wood", 4)
+    L = _lib.lib()
+    z = torch.empty(0, dtype=torch.float64, device="cuda")
+    assert L.nlk_solve_batch(h, 0, 0, 0, z.data_ptr(), None, 1e-8, 1000, z.data_ptr(),
+                             z.data_ptr(), z.data_ptr(), None, None, None, None, None) == 0
+    assert L.nlk_solve_batch_host(h, 0, 0, 0, None, None, 1e-8, 1000, None, None, None, None,
+                                  None, None, None, 0, 0) == 0
+    r = solvers.solve_batch("test23/wood", np.zeros((0, 4)), None, "trust-region", n=4)
+    assert r.u.shape == (0, 4)
+
+
+@pytest.mark.parametrize("B", [1, 31, 33, 127, 129, 4097])
+@pytest.mark.parametrize("alg", ["newton-raphson", "trust-region", "klement"])
+def test_ragged_batches_match_oracle(B, alg):
+    b = W.c2_suite(11, 0, B, 0.1)  # trigonometric, n = 10 (shared-memory LU path)
+    got = _solve(b.problem_id, alg, b.u0, None, 1e-8, 1000)
+    ref = O.solve_batch(b.problem_id, alg, b.u0)
+    for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        assert np.array_equal(got[f], ref[f]), f
+    assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"])
