@@ -17,7 +17,7 @@ Reported on one JSON line (rank 0):
   value    systems solved/s, inputs resident in HBM, CUDA events on the
            launching stream, barrier + synchronize on both sides;
   e2e      same metric through the C-ABI with HOST buffers
-           (nlk_solve_batch_host_async per job on 3 streams: pinned H2D,
+           (nlk_solve_batch_host_async per job on 6 streams: pinned H2D,
            solve, D2H of every output inside the timing);
   roofline dominant kernel: algorithmic FP64 FLOPs (SURVEY.md §8d,
            paper_2403_16341_b200/flops.py) / its CUDA-event duration, against
@@ -319,7 +319,8 @@ def run_ours(args, rank, world, local_rank, dist):
         # every job enqueued through the asynchronous host-buffer entry point,
         # round-robin over 3 streams (copies of one job overlap the solves of
         # others), one synchronisation per step
-        e2e_streams = [torch.cuda.Stream(dev) for _ in range(3)]
+        nst = int(os.environ.get("NLK_E2E_STREAMS", "6"))
+        e2e_streams = [torch.cuda.Stream(dev) for _ in range(nst)]
 
         def e2e_step():
             for j, (h_, a_, Bj, hu0, hp, (uo, ro, rc, cn)) in enumerate(host):
@@ -327,7 +328,7 @@ def run_ours(args, rank, world, local_rank, dist):
                     h_, a_, 0, Bj, hu0.data_ptr(), None if hp is None else hp.data_ptr(), 1e-8,
                     1000, uo.data_ptr(), ro.data_ptr(), rc.data_ptr(), cn[0].data_ptr(),
                     cn[1].data_ptr(), cn[2].data_ptr(), cn[3].data_ptr(),
-                    e2e_streams[j % 3].cuda_stream))
+                    e2e_streams[j % nst].cuda_stream))
             for st_ in e2e_streams:
                 st_.synchronize()
 
@@ -335,17 +336,23 @@ def run_ours(args, rank, world, local_rank, dist):
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
+        step_t = []
         for _ in range(args.e2e_steps):
+            ts = time.perf_counter()
             e2e_step()
+            step_t.append(time.perf_counter() - ts)
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         bi = sum((x[3].numel() + (0 if x[4] is None else x[4].numel())) * 8 for x in host)
         bo = sum(x[5][0].numel() * 8 + x[5][1].numel() * 8 + x[5][2].numel() + x[5][3].numel() * 4
                  for x in host)
-        e2e = {"value": world * per_step_systems * args.e2e_steps / float(te.item()),
+        # value: median step (robust to a one-off host hiccup); value_mean: all steps
+        e2e = {"value": world * per_step_systems / statistics.median(step_t),
+               "value_mean": world * per_step_systems * args.e2e_steps / float(te.item()),
                "unit": "systems/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
-               "steps": args.e2e_steps}
+               "steps": args.e2e_steps, "step_ms": [round(1e3 * t, 1) for t in step_t],
+               "streams": nst}
 
     # roofline.traffic: DRAM bytes of the dominant kernel from a committed ncu --set full
     # capture (profiles/ncu_traffic.json), scaled to this run's batch; null if none matches
@@ -389,7 +396,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=1 << 20, help="systems per job per GPU")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=60, help="systems per job for the CPU leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats", default=None, help="write per-launch stats JSON here")
