@@ -219,6 +219,13 @@ def run_ours(args, rank, world, local_rank, dist):
     L = _lib.lib()
     B = args.batch
     lo, hi = rank * B, (rank + 1) * B
+    f32 = args.dtype == "f32"
+    tdt = torch.float32 if f32 else torch.float64
+    esz = 4 if f32 else 8
+    # fp32 cannot reach 1e-8 on the parametrised quadratics (SURVEY.md §7:
+    # MaxIters on ~95 %); their fp32 runs use 1e-6.  Generalized Rosenbrock's
+    # root is exactly representable, so C3 keeps 1e-8 in fp32.
+    abstol = args.abstol or (1e-6 if f32 and args.config in ("c1", "c5") else 1e-8)
     jobs = jobs_for(args.config, lo, hi)
     if args.only:
         keys = args.only.split(",")
@@ -229,14 +236,14 @@ def run_ours(args, rank, world, local_rank, dist):
     for pid, n, alg, b in jobs:
         key = id(b)
         if key not in inputs:
-            u0 = torch.from_numpy(np.ascontiguousarray(b.u0.T)).to(dev)
-            p = None if b.p is None else torch.from_numpy(np.ascontiguousarray(b.p.T)).to(dev)
+            u0 = torch.from_numpy(np.ascontiguousarray(b.u0.T)).to(dev, tdt)
+            p = None if b.p is None else torch.from_numpy(np.ascontiguousarray(b.p.T)).to(dev, tdt)
             inputs[key] = (u0, p)
         u0, p = inputs[key]
         h, nn, m = _lib.problem_lookup(pid, n)
         Bj = u0.shape[1]
-        out = {"u": torch.empty((n, Bj), dtype=torch.float64, device=dev),
-               "resid": torch.empty(Bj, dtype=torch.float64, device=dev),
+        out = {"u": torch.empty((n, Bj), dtype=tdt, device=dev),
+               "resid": torch.empty(Bj, dtype=tdt, device=dev),
                "retcode": torch.empty(Bj, dtype=torch.int8, device=dev),
                "counters": torch.empty((4, Bj), dtype=torch.int32, device=dev)}
         prepared.append((pid, n, m, alg, h, u0, p, out, b))
@@ -248,12 +255,13 @@ def run_ours(args, rank, world, local_rank, dist):
         for j, (pid, n, m, alg, h, u0, p, out, b) in enumerate(prepared):
             if events is not None:
                 events[j][0].record(stream)
-            solvers.solve_batch_soa(h, ALG_ID[alg], u0, p, 1e-8, 1000, out=out, stream=sptr)
+            solvers.solve_batch_soa(h, ALG_ID[alg], u0, p, abstol, 1000, out=out, stream=sptr)
             if events is not None:
                 events[j][1].record(stream)
 
     peak = ctypes.c_double()
-    _lib.check(L.nlk_fp64_peak(1 << 16, ctypes.byref(peak), ctypes.c_void_p(sptr)))
+    _lib.check((L.nlk_fp32_peak if f32 else L.nlk_fp64_peak)(
+        1 << 16, ctypes.byref(peak), ctypes.c_void_p(sptr)))
     fp64_peak = peak.value
 
     for _ in range(args.warmup):
@@ -294,13 +302,13 @@ def run_ours(args, rank, world, local_rank, dist):
     for (pid_, n_, m_, alg_, _h, _u0, _p, out_, _b) in prepared:
         cc = out_["counters"]
         total_flops += float(flops.system_flops(pid_, n_, alg_, cc[0], cc[1], cc[2], cc[3]).sum())
-    kernel_names = [f"solve_kernel<{x[0]},n={x[1]},{x[3]}>" for x in prepared]
+    kernel_names = [f"solve_kernel<{x[0]},n={x[1]},{x[3]}{',f32' if f32 else ''}>" for x in prepared]
     stats = {"per_launch_ms": dict(zip(kernel_names, [round(v, 4) for v in launch_ms])),
              "retcodes": {kernel_names[j]: np.bincount(prepared[j][7]["retcode"].cpu().numpy(),
                                                        minlength=6).tolist()
                           for j in range(len(prepared))},
              "step_fp64_tflops": total_flops / (elapsed / args.steps) / 1e12}
-    hbm_bytes = sum(flops.system_bytes(x[1], x[2]) * x[5].shape[1] for x in prepared)
+    hbm_bytes = sum(flops.system_bytes(x[1], x[2], elem=esz) * x[5].shape[1] for x in prepared)
 
     # ---- e2e through the C-ABI with host buffers
     e2e = None
@@ -310,8 +318,8 @@ def run_ours(args, rank, world, local_rank, dist):
             hu0 = u0_.cpu().pin_memory()
             hp = None if p_ is None else p_.cpu().pin_memory()
             Bj = hu0.shape[1]
-            hout = (torch.empty((n_, Bj), dtype=torch.float64).pin_memory(),
-                    torch.empty(Bj, dtype=torch.float64).pin_memory(),
+            hout = (torch.empty((n_, Bj), dtype=tdt).pin_memory(),
+                    torch.empty(Bj, dtype=tdt).pin_memory(),
                     torch.empty(Bj, dtype=torch.int8).pin_memory(),
                     torch.empty((4, Bj), dtype=torch.int32).pin_memory())
             host.append((h_, ALG_ID[alg_], Bj, hu0, hp, hout))
@@ -325,7 +333,7 @@ def run_ours(args, rank, world, local_rank, dist):
         def e2e_step():
             for j, (h_, a_, Bj, hu0, hp, (uo, ro, rc, cn)) in enumerate(host):
                 _lib.check(L.nlk_solve_batch_host_async(
-                    h_, a_, 0, Bj, hu0.data_ptr(), None if hp is None else hp.data_ptr(), 1e-8,
+                    h_, a_, 1 if f32 else 0, Bj, hu0.data_ptr(), None if hp is None else hp.data_ptr(), abstol,
                     1000, uo.data_ptr(), ro.data_ptr(), rc.data_ptr(), cn[0].data_ptr(),
                     cn[1].data_ptr(), cn[2].data_ptr(), cn[3].data_ptr(),
                     e2e_streams[j % nst].cuda_stream))
@@ -344,8 +352,8 @@ def run_ours(args, rank, world, local_rank, dist):
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        bi = sum((x[3].numel() + (0 if x[4] is None else x[4].numel())) * 8 for x in host)
-        bo = sum(x[5][0].numel() * 8 + x[5][1].numel() * 8 + x[5][2].numel() + x[5][3].numel() * 4
+        bi = sum((x[3].numel() + (0 if x[4] is None else x[4].numel())) * esz for x in host)
+        bo = sum(x[5][0].numel() * esz + x[5][1].numel() * esz + x[5][2].numel() + x[5][3].numel() * 4
                  for x in host)
         # value: median step (robust to a one-off host hiccup); value_mean: all steps
         e2e = {"value": world * per_step_systems / statistics.median(step_t),
@@ -367,20 +375,21 @@ def run_ours(args, rank, world, local_rank, dist):
         "metric": METRIC, "value": value, "unit": "systems/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "batch_per_job_per_gpu": B,
                    "jobs": len(prepared), "systems_per_step_per_gpu": per_step_systems,
-                   "abstol": 1e-8, "maxiters": 1000,
+                   "abstol": abstol, "maxiters": 1000,
                    "l2": f"inputs+outputs {hbm_bytes / 1e9:.2f} GB/step/GPU > 126 MB L2 (no flush needed)",
                    "parallelism": f"shard{world} (independent systems, no collective)"},
         "gpu_launches": len(prepared) * args.steps,
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
+        "roofline": {"bound": "fp32" if f32 else "fp64", "achieved": achieved, "peak": fp64_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
-                     "algorithmic_bytes": flops.system_bytes(n, m) * prepared[jdom][5].shape[1],
+                     "algorithmic_bytes": flops.system_bytes(n, m, elem=esz) * prepared[jdom][5].shape[1],
                      "kernel": kernel_names[jdom], "launch_ms": launch_ms[jdom],
                      "flops_per_launch": F,
-                     "peak_source": "nlk_fp64_peak (DFMA chains, measured in this run)",
+                     "peak_source": ("nlk_fp32_peak (FFMA chains" if f32 else "nlk_fp64_peak (DFMA chains")
+                                    + ", measured in this run)",
                      "hbm_gbs": hbm_bytes / (elapsed / args.steps) / 1e9},
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -396,6 +405,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=1 << 20, help="systems per job per GPU")
+    ap.add_argument("--abstol", type=float, default=None,
+                    help="default 1e-8 (f32 on the quadratics: 1e-6)")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="arithmetic type (f32: registered fp32 instances, C1/C3/C4/C5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=60, help="systems per job for the CPU leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")

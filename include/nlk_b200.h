@@ -124,6 +124,9 @@ NLK_API int nlk_last_grid(void);
  * The roofline denominator for the solve kernels, which are FP64-issue
  * bound rather than HBM- or tensor-bound. */
 NLK_API int nlk_fp64_peak(int64_t iters, double* tflops_out, void* stream);
+/* The same for the FP32 FMA pipe (FFMA chains): the roofline denominator of
+ * the fp32 instantiations. */
+NLK_API int nlk_fp32_peak(int64_t iters, double* tflops_out, void* stream);
 
 /* Implicit-function-theorem sensitivities at B roots of one parametrised
  * problem (m > 0), device buffers, asynchronous on `stream`.

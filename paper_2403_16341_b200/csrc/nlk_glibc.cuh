@@ -449,6 +449,67 @@ NLK_HD void sincos(double x, double* s, double* c) {
   }
 }
 
+// sincos of G independent arguments, each result bit-identical to sincos()
+// above, written branch-free so that the G dependency chains interleave
+// (one thread evaluates a residual's G transcendentals with G-way ILP instead
+// of G serial calls).  Per argument: the classification of sincos() becomes
+// selects, both sine kernels (Taylor and table) are evaluated and the one
+// glibc would take is kept, and the table index of lanes that take neither
+// is clamped to a valid entry.  Arguments outside the Cody-Waite range
+// (|x| >= 105414350, inf, NaN) are rare: they take the scalar sincos()
+// afterwards: sincos_n returns true when some argument needs that, and the
+// caller re-evaluates those with sincos() (sincos_n leaves them unspecified).
+NLK_HD bool sincos_slow(double x) {
+  return (static_cast<uint32_t>(asu(x) >> 32) & 0x7fffffffu) >= 0x419921fbu;
+}
+template <int G>
+NLK_HD bool sincos_n(const double* x, double* s, double* c) {
+  double as[G], das[G], ac[G], dac[G];
+  int n[G], mode[G];
+  bool slow = false;
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int g = 0; g < G; ++g) {
+    const uint32_t k = static_cast<uint32_t>(asu(x[g]) >> 32) & 0x7fffffffu;
+    const bool big = k >= 0x419921fbu;
+    slow |= big;
+    const double xs = big ? 0.5 : x[g];  // keeps every table index in range
+    double a, da;
+    const int nn = reduce_sincos(xs, &a, &da);
+    const double y = kHp0 - fabs(xs);
+    const double a1 = y + kHp1;
+    const double da1 = (y - a1) + kHp1;
+    const int m = (k < 0x3feb6000u) ? 0 : ((k < 0x400368fdu) ? 1 : 2);
+    mode[g] = m;
+    n[g] = nn;
+    as[g] = m == 0 ? xs : (m == 1 ? a1 : a);
+    das[g] = m == 0 ? 0.0 : (m == 1 ? da1 : da);
+    ac[g] = m == 0 ? xs : (m == 1 ? y : a);
+    dac[g] = m == 0 ? 0.0 : (m == 1 ? kHp1 : da);
+  }
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int g = 0; g < G; ++g) {
+    const double vt = taylor_sin(as[g], das[g]);
+    const double vb = do_sin_tab(as[g], das[g]);
+    const double vs = (fabs(as[g]) < kSmall) ? vt : vb;
+    const double vc = do_cos_tab(ac[g], dac[g]);
+    const uint32_t k = static_cast<uint32_t>(asu(x[g]) >> 32) & 0x7fffffffu;
+    const int nn = n[g];
+    const double rs = (nn & 1) ? vc : vs;
+    const double rc = ((nn + 1) & 1) ? vc : vs;
+    const double s2 = (nn & 2) ? -rs : rs;
+    const double c2 = ((nn + 1) & 2) ? -rc : rc;
+    const double s0 = (k < 0x3e500000u) ? x[g] : vs;
+    const double c0 = (k < 0x3e400000u) ? 1.0 : vc;
+    s[g] = mode[g] == 0 ? s0 : (mode[g] == 1 ? copysign(vc, x[g]) : s2);
+    c[g] = mode[g] == 0 ? c0 : (mode[g] == 1 ? vs : c2);
+  }
+  return slow;
+}
+
 // ---- atan (sysdeps/ieee754/dbl-64/s_atan.c, 2.35+ table version, FMA build) --
 constexpr double kA0 = 0x1.375f08b31cbcep-4, kA1 = -0x1.7458022b13c25p-4;
 constexpr double kA2 = 0x1.c71c6e5129a3bp-4, kA3 = -0x1.24924923f7603p-3;

@@ -93,6 +93,10 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
 // memoised (np.sin/np.cos/x**3 == math.*; np.exp and np.arctan are SVML on
 // float64, not glibc, so exp and atan are not), and only where both paths
 // feed them the same bits.  `kMemo` = slots a residual records per evaluation.
+// arguments per glibc::sincos_n group in Ctx::sincos_all (0: one call each)
+#ifndef NLK_SINCOS_GROUP
+#define NLK_SINCOS_GROUP 0
+#endif
 template <class T, int MODE>
 struct Ctx {
   T* m;
@@ -112,6 +116,38 @@ struct Ctx {
       if constexpr (MODE == 1) { m[i] = value_of(s); m[i + 1] = value_of(c); }
     }
     i += 2;
+  }
+  // sincos of G arguments: the fp64 float path evaluates them together
+  // (glibc::sincos_n, G-way ILP; same bits as G separate calls)
+  template <int G, class S> NLK_FD void sincos_all(const S* x, S* s, S* c) {
+    if constexpr (std::is_same<S, double>::value && NLK_SINCOS_GROUP > 0) {
+      constexpr int GG = NLK_SINCOS_GROUP < G ? NLK_SINCOS_GROUP : G;
+#pragma unroll
+      for (int g0 = 0; g0 < G; g0 += GG) {
+        constexpr int R = G % GG;
+        if (g0 + GG <= G) {
+          if (glibc::sincos_n<GG>(x + g0, s + g0, c + g0)) {
+#pragma unroll
+            for (int g = g0; g < g0 + GG; ++g)
+              if (glibc::sincos_slow(x[g])) t_sincos(x[g], s[g], c[g]);
+          }
+        } else if constexpr (R > 0) {
+          if (glibc::sincos_n<R>(x + g0, s + g0, c + g0)) {
+#pragma unroll
+            for (int g = g0; g < G; ++g)
+              if (glibc::sincos_slow(x[g])) t_sincos(x[g], s[g], c[g]);
+          }
+        }
+      }
+      if constexpr (MODE == 1) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) { m[i + 2 * g] = s[g]; m[i + 2 * g + 1] = c[g]; }
+      }
+      i += 2 * G;
+    } else {
+#pragma unroll
+      for (int g = 0; g < G; ++g) sincos(x[g], s[g], c[g]);
+    }
   }
   template <class S> NLK_FD S cos(const S& x) {
     S s, c;
@@ -300,8 +336,7 @@ struct Trigonometric {  // 171-177
   static constexpr int kMemo = 2 * N;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S c[N], sn[N];  // np.cos(x) and np.sin(x[k]): one sincos per component
-#pragma unroll
-    for (int k = 0; k < N; ++k) cx.sincos(x[k], sn[k], c[k]);
+    cx.template sincos_all<N>(x, sn, c);
     S cos_sum = np_sum<N>(c);
 #pragma unroll
     for (int k = 0; k < N; ++k)

@@ -35,6 +35,11 @@ namespace nlk {
 #define NLK_SMU _Pragma("unroll 1")
 #endif
 
+// 1: getrs substitutes on a register copy of the permuted right-hand side
+#ifndef NLK_GETRS_REG
+#define NLK_GETRS_REG 0
+#endif
+
 #define NLK_FD __device__ __forceinline__
 
 // threads per block of the solve kernel = stride of the per-thread slices
@@ -252,6 +257,25 @@ NLK_SMU
     b.v(i) = b.v(p);
     b.v(p) = t;
   }
+#if NLK_GETRS_REG
+  // the substitutions on a register copy of the permuted right-hand side
+  T x[N];
+NLK_SMU
+  for (int i = 0; i < N; ++i) x[i] = b.v(i);
+NLK_SMU
+  for (int i = 0; i < N; ++i) {
+NLK_SMU
+    for (int r = i + 1; r < N; ++r) x[r] = t_fma(-x[i], LU(r, i), x[r]);
+  }
+NLK_SMU
+  for (int i = N - 1; i >= 0; --i) {
+    x[i] = x[i] / LU(i, i);
+NLK_SMU
+    for (int r = 0; r < i; ++r) x[r] = t_fma(-x[i], LU(r, i), x[r]);
+  }
+NLK_SMU
+  for (int i = 0; i < N; ++i) b.v(i) = x[i];
+#else
 NLK_SMU
   for (int i = 0; i < N; ++i) {
     const T bi = b.v(i);
@@ -265,6 +289,7 @@ NLK_SMU
 NLK_SMU
     for (int r = 0; r < i; ++r) b.v(r) = t_fma(-bi, LU(r, i), b.v(r));
   }
+#endif
 }
 
 // smem path when n >= NLK_SMEM_LU_MIN and the N*N + N slice of a 128-thread

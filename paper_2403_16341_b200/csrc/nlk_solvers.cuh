@@ -232,6 +232,10 @@ struct NewtonRaphson : Base<P, N, T> {
 #ifndef NLK_TR_JSMEM
 #define NLK_TR_JSMEM 0
 #endif
+// keep the dogleg's radius-independent values across rejected steps
+#ifndef NLK_TR_DLCACHE
+#define NLK_TR_DLCACHE 1
+#endif
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
   using B = Base<P, N, T, NLK_TR_MEMO>;
@@ -258,7 +262,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
     return st;
   }
   // dogleg_direction (descent.py:78-106)
-  NLK_FD void dogleg(T* out) {
+  NLK_FD void dogleg_plain(T* out) {
     T newton[N];
     if constexpr (SM) {
       const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
@@ -302,9 +306,89 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
 #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = cauchy[i] + tau * d[i];
   }
+  // The same dogleg with its radius-independent part kept across rejected
+  // steps (shared-memory path, NLK_TR_DLCACHE).  A rejection leaves u, f, J
+  // and the LU unchanged and only shrinks the radius, so the Newton step and
+  // its norm, g = J^T f, J g, the Cauchy point and its norm are the same at
+  // the next iteration; only the radius-dependent tail is re-evaluated, with
+  // the same operations on the same values (bit-identical).  On MaxIters-bound
+  // runs most iterations are rejections (test23/trigonometric, sigma = 0.1:
+  // 94 %).  dl: 0 nothing cached; 1 Newton step in the rhs slot + its norm;
+  // 2 + gg, t_star, |cauchy|; 3 g in the rhs slot instead -- set once the
+  // scaled-gradient branch is taken: the radius only shrinks until the next
+  // accepted step, so the Newton step and the segment are not needed again.
+  // Measured (C2 jobs, B = 2^20): trigonometric 326 -> 283 ms; for the
+  // register path (n < 9) the extra loop-carried state cost more than it
+  // saved (matrix-sqrt-2x2 36 -> 47 ms), so it keeps dogleg_plain.
+  static constexpr bool kDlCache = SM && NLK_TR_DLCACHE;
+  T nnorm, gg, t_star, cnorm;
+  int dl;
+  NLK_FD void dogleg_cached(T* out) {
+    const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
+    if (dl == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
+      sm_getrs<N>(A, piv, rhs);
+      T newton[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) newton[i] = rhs.v(i);
+      nnorm = norm2<N>(newton);
+      dl = 1;
+    }
+    if (dl < 3 && nnorm <= radius) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[i] = rhs.v(i);
+      return;
+    }
+    T g[N];
+    if (dl == 3) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) g[i] = rhs.v(i);
+    } else {
+      gemv_AT_x<N>(jmat(), B::f, g);
+      if (dl == 1) {
+        T Jg[N], cauchy[N];
+        gemv_A_x<N>(jmat(), g, Jg);
+        gg = ddot<N>(g, g);
+        T jj = ddot<N>(Jg, Jg);
+        t_star = gg / ((Num<T>::tiny > jj) ? Num<T>::tiny : jj);
+#pragma unroll
+        for (int i = 0; i < N; ++i) cauchy[i] = -t_star * g[i];
+        cnorm = norm2<N>(cauchy);
+        dl = 2;
+      }
+    }
+    if (cnorm >= radius) {
+      T s = -(radius / sqrt(gg));
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[i] = s * g[i];
+      if (dl == 2) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) rhs.v(i) = g[i];
+        dl = 3;
+      }
+      return;
+    }
+    T cauchy[N], d[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) cauchy[i] = -t_star * g[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = rhs.v(i) - cauchy[i];
+    T a = ddot<N>(d, d);
+    T b = T(2) * ddot<N>(cauchy, d);
+    T c = cnorm * cnorm - radius * radius;
+    T tau = (-b + sqrt(b * b - T(4) * a * c)) / (T(2) * a);
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = cauchy[i] + tau * d[i];
+  }
+  NLK_FD void dogleg(T* out) {
+    if constexpr (kDlCache) dogleg_cached(out);
+    else dogleg_plain(out);
+  }
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
     if (!cached) {
+      if constexpr (kDlCache) dl = 0;
       if (B::jac(jmat()) >= 0) return NONFINITE;
       if constexpr (SM) {
         const SMat<N, T> A{B::sm};

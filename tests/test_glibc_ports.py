@@ -19,6 +19,12 @@ extern "C" {
 void g_exp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::exp(x[i]); }
 void g_sincos_s(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) { double c; nlk::glibc::sincos(x[i], &y[i], &c); } }
 void g_sincos_c(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) { double s; nlk::glibc::sincos(x[i], &s, &y[i]); } }
+void g_sincosn(const double* x, double* s, double* c, long n) {  // n % 10 == 0
+  for (long i = 0; i < n; i += 10)
+    if (nlk::glibc::sincos_n<10>(x + i, s + i, c + i))
+      for (long j = i; j < i + 10; ++j)
+        if (nlk::glibc::sincos_slow(x[j])) nlk::glibc::sincos(x[j], &s[j], &c[j]);
+}
 void g_npexp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::svml::exp(x[i]); }
 void g_npatan(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::svml::atan(x[i]); }
 void g_sin(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = nlk::glibc::sin(x[i]); }
@@ -114,3 +120,20 @@ def test_numpy_arctan_port_is_bit_exact(lib):
     ref = np.arctan(x)
     same = (a.view(np.int64) == ref.view(np.int64)) | (np.isnan(a) & np.isnan(ref))
     assert same.all(), f"{np.count_nonzero(~same)} mismatches, e.g. x={x[~same][:4]}"
+
+
+def test_grouped_sincos_is_bit_exact(lib):
+    """glibc::sincos_n (the branch-free G-argument form the fp64 residuals
+    use) equals libm sin and cos on every branch, arguments mixed per group."""
+    rng = np.random.default_rng(9)
+    x = np.concatenate([inputs("sin", 100_000, rng), inputs("cos", 100_000, rng)])
+    x = rng.permutation(x)
+    x = np.ascontiguousarray(np.concatenate([x, np.zeros((-len(x)) % 10)]))
+    s, c, rs, rc = (np.empty_like(x) for _ in range(4))
+    ptr = lambda v: v.ctypes.data_as(ctypes.c_void_p)
+    lib.g_sincosn(ptr(x), ptr(s), ptr(c), ctypes.c_long(len(x)))
+    lib.l_sin(ptr(x), ptr(rs), ctypes.c_long(len(x)))
+    lib.l_cos(ptr(x), ptr(rc), ctypes.c_long(len(x)))
+    for a, b in ((s, rs), (c, rc)):
+        same = (a.view(np.int64) == b.view(np.int64)) | (np.isnan(a) & np.isnan(b))
+        assert same.all(), f"{np.count_nonzero(~same)} mismatches, e.g. x={x[~same][:3]}"
