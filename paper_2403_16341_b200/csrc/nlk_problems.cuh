@@ -169,6 +169,11 @@ struct Ctx {
     return r;
   }
 };
+template <class P, class = void> struct JacRankOneDiag { static constexpr bool value = false; };
+template <class P>
+struct JacRankOneDiag<P, std::void_t<decltype(P::kJacRankOneDiag)>> {
+  static constexpr bool value = P::kJacRankOneDiag;
+};
 template <class P, class = void> struct MemoOf { static constexpr int value = 0; };
 template <class P> struct MemoOf<P, std::void_t<decltype(P::kMemo)>> { static constexpr int value = P::kMemo; };
 
@@ -334,6 +339,13 @@ struct DiscreteIntegral {  // 154-168
 struct Trigonometric {  // 171-177
   static constexpr int N = 10, M = 0;
   static constexpr int kMemo = 2 * N;
+  // Jacobian structure: column j off the diagonal is d(n - cos_sum)/dx_j
+  // plus exact zeros, so every off-diagonal entry of a column has the same
+  // bits, except that the entries of an all-zero column (x_j = +-0) carry
+  // row-dependent zero signs (checked against the reference's dense_jacobian
+  // on 3,000 points incl. zeros).  Drivers that keep J may store it as
+  // diagonal + one value per column + zero signs (RDJac, nlk_solvers.cuh).
+  static constexpr bool kJacRankOneDiag = true;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S c[N], sn[N];  // np.cos(x) and np.sin(x[k]): one sincos per component
     cx.template sincos_all<N>(x, sn, c);

@@ -65,6 +65,53 @@ template <int N> struct SweepWidth {
 template <class T> NLK_FD void jput(T* J, int e, T v) { J[e] = v; }
 template <int N, class T> NLK_FD void jput(const SMat<N, T>& J, int e, T v) { J.v(e) = v; }
 
+// A Jacobian whose off-diagonal entries of each column share one value
+// (problems with kJacRankOneDiag): diagonal d, column values s, and the
+// zero signs of the off-diagonal entries (only an all-zero column can carry
+// different bits per row).  2N values + N*N bits instead of N*N values.
+// Accessors rebuild every entry bit-exactly; ZS = false skips the zero-sign
+// lookup (valid when no column value is zero, i.e. !zany).
+template <int N, class T>
+struct RDJac {
+  T d[N], s[N];
+  uint32_t zm[(N * N + 31) / 32];
+  bool zany;
+  NLK_FD void reset() {
+#pragma unroll
+    for (int w = 0; w < (N * N + 31) / 32; ++w) zm[w] = 0u;
+    zany = false;
+  }
+};
+template <int N, class T, bool ZS>
+struct RDRef {
+  RDJac<N, T>* J;
+};
+template <int N, class T, bool ZS>
+NLK_FD T mat_at(const RDRef<N, T, ZS>& A, int e) {
+  const int i = e % N, j = e / N;
+  if (i == j) return A.J->d[i];
+  if constexpr (!ZS) {
+    return A.J->s[j];
+  } else {
+    const T v = A.J->s[j];
+    const bool neg = (A.J->zm[e >> 5] >> (e & 31)) & 1u;
+    return (v != T(0)) ? v : (neg ? -T(0) : T(0));
+  }
+}
+template <int N, class T, bool ZS>
+NLK_FD void jput(const RDRef<N, T, ZS>& A, int e, T v) {
+  const int i = e % N, j = e / N;
+  if (i == j) {
+    A.J->d[i] = v;
+    return;
+  }
+  if (i == (j == 0 ? 1 : 0)) {
+    A.J->s[j] = v;
+    A.J->zany |= (v == T(0));
+  }
+  if (v == T(0) && signbit(v)) A.J->zm[e >> 5] |= 1u << (e & 31);
+}
+
 // dense_jacobian (autodiff.py:342-355) into column-major J.  Returns -1 on
 // success, else the index of the reference chunk (8 columns) whose check
 // raised NonFiniteValue — nlkit evaluates chunks up to and including it.
@@ -244,10 +291,28 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
   static constexpr bool JSM =
       SM && NLK_TR_JSMEM && sizeof(T) * (2 * N * N + N) * kSmStride <= 227 * 1024;
   static constexpr int kSmemElems = SM ? (JSM ? 2 * N * N + N : N * N + N) : 0;
-  T J[JSM ? 1 : N * N], LU[SM ? 1 : N * N];
+  // RD: a rank-one-plus-diagonal Jacobian kept as RDJac (2N values instead of
+  // N^2 registers; test23/trigonometric: the cached J was what spilled)
+#ifndef NLK_TR_RDJAC
+#define NLK_TR_RDJAC 1
+#endif
+  static constexpr bool RD = !JSM && NLK_TR_RDJAC && JacRankOneDiag<P>::value;
+  T J[(JSM || RD) ? 1 : N * N], LU[SM ? 1 : N * N];
+  RDJac<N, T> jrd[RD ? 1 : 0];
   NLK_FD auto jmat() {
     if constexpr (JSM) return SMat<N, T>{B::sm + (N * N + N) * kSmStride};
+    else if constexpr (RD) return RDRef<N, T, true>{&jrd[0]};
     else return static_cast<T*>(J);
+  }
+  // f(J accessor); for RD the zero-sign lookups are skipped unless some
+  // column value is zero
+  template <class F> NLK_FD void with_j(F&& f) {
+    if constexpr (RD) {
+      if (jrd[0].zany) f(RDRef<N, T, true>{&jrd[0]});
+      else f(RDRef<N, T, false>{&jrd[0]});
+    } else {
+      f(jmat());
+    }
   }
   int piv[N];
   T radius, radius_max;
@@ -282,8 +347,10 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
       return;
     }
     T g[N], Jg[N], cauchy[N];
-    gemv_AT_x<N>(jmat(), B::f, g);
-    gemv_A_x<N>(jmat(), g, Jg);
+    with_j([&](auto Jm) {
+      gemv_AT_x<N>(Jm, B::f, g);
+      gemv_A_x<N>(Jm, g, Jg);
+    });
     T gg = ddot<N>(g, g);
     T jj = ddot<N>(Jg, Jg);
     T t_star = gg / ((Num<T>::tiny > jj) ? Num<T>::tiny : jj);
@@ -345,10 +412,10 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
 #pragma unroll
       for (int i = 0; i < N; ++i) g[i] = rhs.v(i);
     } else {
-      gemv_AT_x<N>(jmat(), B::f, g);
+      with_j([&](auto Jm) { gemv_AT_x<N>(Jm, B::f, g); });
       if (dl == 1) {
         T Jg[N], cauchy[N];
-        gemv_A_x<N>(jmat(), g, Jg);
+        with_j([&](auto Jm) { gemv_A_x<N>(Jm, g, Jg); });
         gg = ddot<N>(g, g);
         T jj = ddot<N>(Jg, Jg);
         t_star = gg / ((Num<T>::tiny > jj) ? Num<T>::tiny : jj);
@@ -389,15 +456,20 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
     B::k += 1;
     if (!cached) {
       if constexpr (kDlCache) dl = 0;
+      if constexpr (RD) jrd[0].reset();
       if (B::jac(jmat()) >= 0) return NONFINITE;
       if constexpr (SM) {
         const SMat<N, T> A{B::sm};
+        with_j([&](auto Jm) {
 #pragma unroll
-        for (int e = 0; e < N * N; ++e) A.v(e) = mat_at(jmat(), e);
+          for (int e = 0; e < N * N; ++e) A.v(e) = mat_at(Jm, e);
+        });
         if (!sm_lu_factor<N, true>(A, piv)) return LINSOLVE_FAILED;
       } else {
+        with_j([&](auto Jm) {
 #pragma unroll
-        for (int i = 0; i < N * N; ++i) LU[i] = J[i];
+          for (int e = 0; e < N * N; ++e) LU[e] = mat_at(Jm, e);
+        });
         if (!lu_factor<N>(LU, piv)) return LINSOLVE_FAILED;
       }
       cached = true;
@@ -413,7 +485,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
     T rho;
     if (all_finite<N>(ft)) {  // tr_ratio (globalize.py:121-134)
       T Jdu[N], model[N];
-      gemv_A_x<N>(jmat(), du, Jdu);
+      with_j([&](auto Jm) { gemv_A_x<N>(Jm, du, Jdu); });
 #pragma unroll
       for (int i = 0; i < N; ++i) model[i] = B::f[i] + Jdu[i];
       T ff = ddot<N>(B::f, B::f);

@@ -66,3 +66,36 @@ def test_ragged_batches_match_oracle(B, alg):
     for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
         assert np.array_equal(got[f], ref[f]), f
     assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"])
+
+
+ZERO = np.load(os.path.join(HERE, "trig_zero.npz"))
+
+
+@pytest.mark.parametrize("alg", ["trust-region", "newton-raphson"])
+def test_trig_zero_components_match_reference(alg):
+    """Exact +-0 start components give all-zero Jacobian columns whose zero
+    signs differ by row: the trust region's compressed Jacobian (RDJac) must
+    rebuild them bit for bit (tests/golden/trig_zero.npz, from the reference)."""
+    g = {x: ZERO[f"{alg}/{x}"] for x in ("u0", "u", "resid", "retcode", "nsteps", "nf", "njac",
+                                          "nlinsolve")}
+    got = _solve("test23/trigonometric", alg, g["u0"], None, 1e-8, 1000)
+    for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        assert np.array_equal(got[f], g[f]), f
+    assert _same(got["u"], g["u"]) and _same(got["resid"], g["resid"])
+
+
+def test_trig_zero_components_match_oracle():
+    """4,096 trigonometric starts with 1-4 exact +-0 components, every
+    algorithm that keeps a Jacobian, bit-identical to the oracle."""
+    rng = np.random.default_rng(5)
+    b = W.c2_suite(11, 0, 4096, 0.1)
+    u0 = b.u0.copy()
+    for i in range(len(u0)):
+        cols = rng.choice(10, 1 + i % 4, replace=False)
+        u0[i, cols] = np.where(np.arange(len(cols)) % 2 == 0, 0.0, -0.0)
+    for alg in ("trust-region", "newton-raphson", "newton-backtracking"):
+        got = _solve("test23/trigonometric", alg, u0, None, 1e-8, 1000)
+        ref = O.solve_batch("test23/trigonometric", alg, u0, None)
+        for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+            assert np.array_equal(got[f], ref[f]), (alg, f)
+        assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg

@@ -34,3 +34,19 @@ def test_oracle_edge_case(case):
     assert ((_bits(r["u"]) == _bits(g["u"])) | both_nan).all()
     rn = np.isnan(r["resid"]) & np.isnan(g["resid"])
     assert ((_bits(r["resid"]) == _bits(g["resid"])) | rn).all()
+
+
+ZERO = np.load(os.path.join(HERE, "trig_zero.npz"))
+
+
+@pytest.mark.parametrize("alg", ["trust-region", "newton-raphson"])
+def test_oracle_trig_zero_components(alg):
+    """Trigonometric starts with exact +-0 components (all-zero Jacobian
+    columns with row-dependent zero signs; make_golden_trig_zero.py)."""
+    g = {x: ZERO[f"{alg}/{x}"] for x in ("u0", "u", "resid", "retcode", "nsteps", "nf", "njac",
+                                          "nlinsolve")}
+    r = O.solve_batch("test23/trigonometric", alg, g["u0"], None, threads=1)
+    for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        assert np.array_equal(r[f], g[f]), f
+    assert (_bits(r["u"]) == _bits(g["u"])).all()
+    assert (_bits(r["resid"]) == _bits(g["resid"])).all()
