@@ -251,13 +251,29 @@ def run_ours(args, rank, world, local_rank, dist):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
+    # --streams K: jobs round-robin over K streams (K = 1: one stream), so the
+    # heavy-tailed end of one persistent launch overlaps the next launch
+    side = [torch.cuda.Stream(dev) for _ in range(max(args.streams, 1) - 1)]
+    lanes = [stream] + side
+
     def one_step(events=None):
+        if side:
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            for st_ in side:
+                st_.wait_event(fork)
         for j, (pid, n, m, alg, h, u0, p, out, b) in enumerate(prepared):
+            st_ = lanes[j % len(lanes)]
             if events is not None:
-                events[j][0].record(stream)
-            solvers.solve_batch_soa(h, ALG_ID[alg], u0, p, abstol, 1000, out=out, stream=sptr)
+                events[j][0].record(st_)
+            solvers.solve_batch_soa(h, ALG_ID[alg], u0, p, abstol, 1000, out=out,
+                                    stream=st_.cuda_stream)
             if events is not None:
-                events[j][1].record(stream)
+                events[j][1].record(st_)
+        for st_ in side:
+            join = torch.cuda.Event()
+            join.record(st_)
+            stream.wait_event(join)
 
     peak = ctypes.c_double()
     _lib.check((L.nlk_fp32_peak if f32 else L.nlk_fp64_peak)(
@@ -313,21 +329,30 @@ def run_ours(args, rank, world, local_rank, dist):
     # ---- e2e through the C-ABI with host buffers
     e2e = None
     if args.e2e_steps > 0:
+        # a job is handed to the library as `pieces` contiguous column chunks
+        # (each its own asynchronous call) when there are fewer jobs than
+        # streams, so that the copies of one chunk overlap the solve of another
+        nst = int(os.environ.get("NLK_E2E_STREAMS", "6"))
+        pieces = max(1, -(-nst // len(prepared)))
         host = []
         for pid_, n_, m_, alg_, h_, u0_, p_, out_, b_ in prepared:
-            hu0 = u0_.cpu().pin_memory()
-            hp = None if p_ is None else p_.cpu().pin_memory()
-            Bj = hu0.shape[1]
-            hout = (torch.empty((n_, Bj), dtype=tdt).pin_memory(),
-                    torch.empty(Bj, dtype=tdt).pin_memory(),
-                    torch.empty(Bj, dtype=torch.int8).pin_memory(),
-                    torch.empty((4, Bj), dtype=torch.int32).pin_memory())
-            host.append((h_, ALG_ID[alg_], Bj, hu0, hp, hout))
+            Bj = u0_.shape[1]
+            bounds = np.linspace(0, Bj, pieces + 1).astype(int)
+            for lo_, hi_ in zip(bounds[:-1], bounds[1:]):
+                if hi_ <= lo_:
+                    continue
+                hu0 = u0_[:, lo_:hi_].contiguous().cpu().pin_memory()
+                hp = None if p_ is None else p_[:, lo_:hi_].contiguous().cpu().pin_memory()
+                Bc = int(hi_ - lo_)
+                hout = (torch.empty((n_, Bc), dtype=tdt).pin_memory(),
+                        torch.empty(Bc, dtype=tdt).pin_memory(),
+                        torch.empty(Bc, dtype=torch.int8).pin_memory(),
+                        torch.empty((4, Bc), dtype=torch.int32).pin_memory())
+                host.append((h_, ALG_ID[alg_], Bc, hu0, hp, hout))
 
-        # every job enqueued through the asynchronous host-buffer entry point,
-        # round-robin over 3 streams (copies of one job overlap the solves of
-        # others), one synchronisation per step
-        nst = int(os.environ.get("NLK_E2E_STREAMS", "6"))
+        # every job (chunk) enqueued through the asynchronous host-buffer entry
+        # point, round-robin over the streams (copies of one overlap the solves
+        # of others), one synchronisation per step
         e2e_streams = [torch.cuda.Stream(dev) for _ in range(nst)]
 
         def e2e_step():
@@ -360,7 +385,7 @@ def run_ours(args, rank, world, local_rank, dist):
                "value_mean": world * per_step_systems * args.e2e_steps / float(te.item()),
                "unit": "systems/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "steps": args.e2e_steps, "step_ms": [round(1e3 * t, 1) for t in step_t],
-               "streams": nst}
+               "streams": nst, "calls_per_step": len(host)}
 
     # roofline.traffic: DRAM bytes of the dominant kernel from a committed ncu --set full
     # capture (profiles/ncu_traffic.json), scaled to this run's batch; null if none matches
@@ -410,6 +435,8 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
                     help="arithmetic type (f32: registered fp32 instances, C1/C3/C4/C5)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--streams", type=int, default=1,
+                    help="device-resident step: jobs round-robin over this many streams")
     ap.add_argument("--cpu-sample", type=int, default=60, help="systems per job for the CPU leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats", default=None, help="write per-launch stats JSON here")

@@ -65,14 +65,59 @@ NLK_SMU
   }
 }
 
-// GETF2 on rows OFF..N-1, columns OFF..OFF+NC-1; piv holds absolute rows
+// Row interchanges as one gather (NLK_LU_GATHER, default on).  A sequence of
+// interchanges applied to a column one after the other is a chain of
+// dependent shared-memory loads and stores with data-dependent addresses
+// (any two may alias) -- ncu put ~20 % of the matrix-sqrt-3x3 trust region's
+// stall samples on those lines.  The same data movement as one gather: the
+// composed permutation is kept as packed 4-bit row indices (n <= 16), row r of
+// the permuted column is row perm_get(R, r) of the stored one, so the N loads
+// are independent and the stores go to static addresses.  Values move, none
+// is computed: bit-identical by construction.
+#ifndef NLK_LU_GATHER
+#define NLK_LU_GATHER 1
+#endif
+template <int N> NLK_FD constexpr uint64_t perm_identity() {
+  uint64_t r = 0;
+  for (int i = 0; i < N; ++i) r |= static_cast<uint64_t>(i) << (4 * i);
+  return r;
+}
+NLK_FD int perm_get(uint64_t R, int i) { return static_cast<int>((R >> (4 * i)) & 15u); }
+// R after interchanging positions i and p
+NLK_FD uint64_t perm_swap(uint64_t R, int i, int p) {
+  const uint64_t x = ((R >> (4 * i)) ^ (R >> (4 * p))) & 15u;
+  return R ^ (x << (4 * i)) ^ (x << (4 * p));
+}
+// the interchanges of A followed by those of B: (A o B)[r] = A[B[r]]
+template <int N> NLK_FD uint64_t perm_compose(uint64_t A, uint64_t B) {
+  uint64_t r = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r |= static_cast<uint64_t>(perm_get(A, perm_get(B, i))) << (4 * i);
+  return r;
+}
+// rows r0..N-1 of column c <- rows perm_get(R, r) (rows below r0 are fixed)
 template <int N, class T>
-NLK_FD void sm_getf2(const SMat<N, T>& A, int OFF, int NC, int* piv) {
+NLK_FD void sm_gather_col(const SMat<N, T>& A, uint64_t R, int r0, int c) {
+  T col[N];
+NLK_SMU
+  for (int r = r0; r < N; ++r) col[r] = A(perm_get(R, r), c);
+NLK_SMU
+  for (int r = r0; r < N; ++r) A(r, c) = col[r];
+}
+
+// GETF2 on rows OFF..N-1, columns OFF..OFF+NC-1; piv holds absolute rows.
+// Returns the panel's interchanges composed (perm_* form).
+template <int N, class T>
+NLK_FD uint64_t sm_getf2(const SMat<N, T>& A, int OFF, int NC, int* piv) {
   const int M = N - OFF;
+  uint64_t R = perm_identity<N>();
 NLK_SMU
   for (int j = 0; j < NC; ++j) {
     const int c = OFF + j;
     // 1. earlier interchanges of this panel, applied to column c
+#if NLK_LU_GATHER
+    if (j > 0) sm_gather_col(A, R, OFF, c);
+#else
 NLK_SMU
     for (int i = 0; i < j; ++i) {
       const int p = piv[OFF + i];  // p == row: a no-op swap (branch-free)
@@ -80,6 +125,7 @@ NLK_SMU
       A(OFF + i, c) = A(p, c);
       A(p, c) = t;
     }
+#endif
     // 2. rows 1..j-1: b_i -= sdot(L[i, 0:i], b[0:i])
 NLK_SMU
     for (int i = 1; i < j; ++i) {
@@ -141,6 +187,7 @@ NLK_SMU
       if (v > best) { best = v; p = r; }
     }
     piv[c] = p;
+    R = perm_swap(R, c, p);
     // 5. interchange over the finished panel columns and b, then scale
     if (best != T(0)) {  // == (A(p, c) != 0): best is |A(p, c)| (NaN included)
       sm_swap_rows(A, c, p, OFF, c + 1);
@@ -152,6 +199,7 @@ NLK_SMU
       }
     }
   }
+  return R;
 }
 
 // C(rows r0.., cols c0..) -= A(rows r0.., cols k0..k0+KK) * B(rows k0.., cols c0..)
@@ -197,18 +245,36 @@ NLK_FD void sm_getrf(const SMat<N, T>& A, int* piv) {
   if constexpr (BLK <= 4) {
     sm_getf2(A, 0, N, piv);
   } else {
+    constexpr int NP = (N + BLK - 1) / BLK;
+    uint64_t Rp[NP];  // each panel's interchanges, composed
 NLK_SMU
     for (int is = 0; is < N; is += BLK) {
       const int bk = (N - is) < BLK ? (N - is) : BLK;
-      sm_getf2(A, is, bk, piv);  // panels of n <= 16 are always GETF2
+      Rp[is / BLK] = sm_getf2(A, is, bk, piv);  // panels of n <= 16 are always GETF2
       if (is + bk < N) {
+#if NLK_LU_GATHER
+NLK_SMU
+        for (int k = is + bk; k < N; ++k) sm_gather_col(A, Rp[is / BLK], is, k);
+#else
 NLK_SMU
         for (int i = is; i < is + bk; ++i)
           sm_swap_rows(A, i, piv[i], is + bk, N);
+#endif
         sm_trsm(A, is, bk);
         sm_gemm_minus(A, is + bk, N - is - bk, is + bk, N - is - bk, is, bk);
       }
     }
+#if NLK_LU_GATHER
+    // later panels' interchanges applied to each earlier panel's columns
+    uint64_t Rl = perm_identity<N>();
+NLK_SMU
+    for (int q = NP - 1; q >= 1; --q) {
+      Rl = perm_compose<N>(Rp[q], Rl);
+      const int is = (q - 1) * BLK;
+NLK_SMU
+      for (int k = is; k < is + BLK; ++k) sm_gather_col(A, Rl, q * BLK, k);
+    }
+#else
 NLK_SMU
     for (int is = 0; is < N; is += BLK) {
       const int bk = (N - is) < BLK ? (N - is) : BLK;
@@ -216,6 +282,7 @@ NLK_SMU
       for (int i = is + bk; i < N; ++i)
         sm_swap_rows(A, i, piv[i], is, is + bk);
     }
+#endif
   }
 }
 
@@ -250,6 +317,18 @@ NLK_SMU
 // getrs with the right-hand side in the strided vector b (N elements)
 template <int N, class T>
 NLK_FD void sm_getrs(const SMat<N, T>& LU, const int* piv, const SMat<N, T>& b) {
+#if NLK_LU_GATHER
+  {
+    uint64_t R = perm_identity<N>();
+#pragma unroll
+    for (int i = 0; i < N; ++i) R = perm_swap(R, i, piv[i]);
+    T x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = b.v(perm_get(R, i));
+#pragma unroll
+    for (int i = 0; i < N; ++i) b.v(i) = x[i];
+  }
+#else
 NLK_SMU
   for (int i = 0; i < N; ++i) {
     const int p = piv[i];
@@ -257,6 +336,7 @@ NLK_SMU
     b.v(i) = b.v(p);
     b.v(p) = t;
   }
+#endif
 #if NLK_GETRS_REG
   // the substitutions on a register copy of the permuted right-hand side
   T x[N];
