@@ -67,7 +67,19 @@ NLK_TRANS_ATTR float nlk_cos(float x) { return cosf(x); }
 NLK_TRANS_ATTR double nlk_atan(double x) { return glibc::atan(x); }      // math.atan (Dual path)
 NLK_TRANS_ATTR double nlk_np_atan(double x) { return svml::atan(x); }  // np.arctan on float64
 NLK_TRANS_ATTR double nlk_pow2(double x) { return glibc::pow_int<2>(x); }
-NLK_TRANS_ATTR void nlk_sincos(double x, double* s, double* c) { glibc::sincos(x, s, c); }
+// sin and cos returned by value (registers): through pointers the call
+// became two local-memory stores in the callee and two loads in the caller
+struct SinCos { double s, c; };
+NLK_TRANS_ATTR SinCos nlk_sincos_v(double x) {
+  SinCos r;
+  glibc::sincos(x, &r.s, &r.c);
+  return r;
+}
+__device__ __forceinline__ void nlk_sincos(double x, double* s, double* c) {
+  const SinCos r = nlk_sincos_v(x);
+  *s = r.s;
+  *c = r.c;
+}
 NLK_TRANS_ATTR void nlk_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
 NLK_TRANS_ATTR double nlk_pow3(double x) { return glibc::pow_int<3>(x); }
 NLK_TRANS_ATTR float nlk_atan(float x) { return atanf(x); }
