@@ -77,6 +77,11 @@ NLK_SMU
 #ifndef NLK_LU_GATHER
 #define NLK_LU_GATHER 1
 #endif
+// 1: the pivot search, interchange and scaling of the current column work on
+// a register copy of it (no data-dependent reload after the search)
+#ifndef NLK_LU_PIVREG
+#define NLK_LU_PIVREG 0
+#endif
 template <int N> NLK_FD constexpr uint64_t perm_identity() {
   uint64_t r = 0;
   for (int i = 0; i < N; ++i) r |= static_cast<uint64_t>(i) << (4 * i);
@@ -178,6 +183,38 @@ NLK_SMU
         A(r, c) = y;
       }
     }
+#if NLK_LU_PIVREG
+    // 4. pivot: first index of max |b[j:]|, on a register copy of b[j:]
+    //    (the pivot value comes out of the search, so the interchange of b
+    //    and its scaling need no data-dependent shared-memory load)
+    T colv[N];
+NLK_SMU
+    for (int r = c; r < N; ++r) colv[r] = A(r, c);
+    int p = c;
+    T best = fabs(colv[c]), pv = colv[c];
+NLK_SMU
+    for (int r = c + 1; r < N; ++r) {
+      T v = fabs(colv[r]);
+      if (v > best) { best = v; p = r; pv = colv[r]; }
+    }
+    piv[c] = p;
+    R = perm_swap(R, c, p);
+    // 5. interchange over the finished panel columns and b, then scale
+    if (best != T(0)) {  // == (A(p, c) != 0): best is |A(p, c)| (NaN included)
+      sm_swap_rows(A, c, p, OFF, c);
+      T outv[N];
+      outv[c] = pv;  // bj: the old A(p, c)
+NLK_SMU
+      for (int r = c + 1; r < N; ++r) outv[r] = (r == p) ? colv[c] : colv[r];
+      if (fabs(pv) >= Num<T>::dbl_min) {
+        const T rr = T(1) / pv;
+NLK_SMU
+        for (int r = c + 1; r < N; ++r) outv[r] = outv[r] * rr;
+      }
+NLK_SMU
+      for (int r = c; r < N; ++r) A(r, c) = outv[r];
+    }
+#else
     // 4. pivot: first index of max |b[j:]|
     int p = c;
     T best = fabs(A(c, c));
@@ -198,6 +235,7 @@ NLK_SMU
         for (int r = c + 1; r < N; ++r) A(r, c) = A(r, c) * rr;
       }
     }
+#endif
   }
   return R;
 }
