@@ -346,6 +346,24 @@ struct Trigonometric {  // 171-177
   // on 3,000 points incl. zeros).  Drivers that keep J may store it as
   // diagonal + one value per column + zero signs (RDJac, nlk_solvers.cuh).
   static constexpr bool kJacRankOneDiag = true;
+  // The dual sweep's Jacobian in closed form, from the memo of F(u)
+  // (memo[2j] = sin u_j, memo[2j+1] = cos u_j).  Column j of the sweep:
+  // d(cos_sum) = -sin u_j exactly (one nonzero term among exact zeros), so
+  // T(N) - cos_sum gives sin u_j; off the diagonal the other terms add exact
+  // zeros, on it (j+1)*(-(-sin u_j)) and -cos u_j are added in the sweep's
+  // order: d_j = (s_j + (j+1)*s_j) - c_j.  With s_j == 0 the zeros' signs
+  // matter: decline, and the sweeps run.
+  template <class T> NLK_FD static bool jac_closed_form(const T* memo, T* d, T* s) {
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const T sj = memo[2 * j], cj = memo[2 * j + 1];
+      ok &= (sj != T(0));
+      s[j] = sj;
+      d[j] = (sj + T(j + 1) * sj) - cj;
+    }
+    return ok;
+  }
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S c[N], sn[N];  // np.cos(x) and np.sin(x[k]): one sincos per component
     cx.template sincos_all<N>(x, sn, c);

@@ -150,8 +150,28 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* memo, JS J, bool& vals_ok, int
 }
 
 // KM > 0: memo holds the KM transcendental values of F(u) (replayed)
+// Problems with an exact closed form of their dual-sweep Jacobian
+// (P::jac_closed_form, fed by the memo of F(u)) skip the sweeps when it
+// applies; it must return the sweeps' bits or decline (return false).
+template <class P, class = void> struct HasJacClosedForm { static constexpr bool value = false; };
+template <class P>
+struct HasJacClosedForm<P, std::void_t<decltype(&P::template jac_closed_form<double>)>> {
+  static constexpr bool value = true;
+};
+#ifndef NLK_JAC_CLOSED_FORM
+#define NLK_JAC_CLOSED_FORM 1
+#endif
+
 template <class P, int N, class T, int KM, class JS>
 NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
+  if constexpr (NLK_JAC_CLOSED_FORM && KM > 0 && HasJacClosedForm<P>::value) {
+    T d[N], sv[N];
+    if (P::template jac_closed_form<T>(memo, d, sv)) {
+#pragma unroll
+      for (int e = 0; e < N * N; ++e) jput(J, e, (e % N == e / N) ? d[e % N] : sv[e / N]);
+      return -1;
+    }
+  }
   bool vals_ok = true;
   int bad_col = N;
   jac_sweeps<P, N, T, KM, 0>(u, p, memo, J, vals_ok, bad_col);
