@@ -352,17 +352,23 @@ struct Trigonometric {  // 171-177
   // T(N) - cos_sum gives sin u_j; off the diagonal the other terms add exact
   // zeros, on it (j+1)*(-(-sin u_j)) and -cos u_j are added in the sweep's
   // order: d_j = (s_j + (j+1)*s_j) - c_j.  With s_j == 0 the zeros' signs
-  // matter: decline, and the sweeps run.
-  template <class T> NLK_FD static bool jac_closed_form(const T* memo, T* d, T* s) {
+  // matter: decline, and the sweeps run.  (The sweep's value path is bounded:
+  // always finite.)
+  static constexpr bool kJacClosedForm = true;
+  template <class T, class PUT>
+  NLK_FD static bool jac_closed_form(const T*, const T* memo, PUT&& put) {
     bool ok = true;
+#pragma unroll
+    for (int j = 0; j < N; ++j) ok &= (memo[2 * j] != T(0));
+    if (!ok) return false;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       const T sj = memo[2 * j], cj = memo[2 * j + 1];
-      ok &= (sj != T(0));
-      s[j] = sj;
-      d[j] = (sj + T(j + 1) * sj) - cj;
+      const T dj = (sj + T(j + 1) * sj) - cj;
+#pragma unroll
+      for (int i = 0; i < N; ++i) put(i + j * N, i == j ? dj : sj);
     }
-    return ok;
+    return true;
   }
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S c[N], sn[N];  // np.cos(x) and np.sin(x[k]): one sincos per component
@@ -429,6 +435,46 @@ struct MatrixSqrt2x2 {  // 213-220
 };
 struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
   static constexpr int N = 9, M = 0;
+  // The dual sweep's Jacobian in closed form.  Entry (row i*3+j, column
+  // a*3+b) of the object matmul's sweep is sum_l (X_il*[l==a][j==b] +
+  // X_lj*[i==a][l==b]) with every product formed (v*1 or v*0) and summed over
+  // l in order.  With every X entry nonzero the nonzero terms are exact and
+  // the zeros cannot change them: j==b, i!=a -> X_ia; i==a, j!=b -> X_bj;
+  // i==a, j==b -> X_aa + X_bb (a == b: X_aa + X_aa); otherwise all six
+  // products are zeros carrying the signs of X_il and X_lj, and the sum is
+  // -0 iff row i and column j of X are all negative.  Declines (sweeps run)
+  // when an entry is zero, or large enough for the sweep's value path to
+  // overflow where the float path did not.
+  static constexpr bool kJacClosedForm = true;
+  template <class T, class PUT>
+  NLK_FD static bool jac_closed_form(const T* x, const T*, PUT&& put) {
+    bool ok = true;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) ok &= (x[e] != T(0)) && (fabs(x[e]) < T(1e150));
+    if (!ok) return false;
+    bool rneg[3], cneg[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      rneg[i] = signbit(x[i * 3 + 0]) && signbit(x[i * 3 + 1]) && signbit(x[i * 3 + 2]);
+      cneg[i] = signbit(x[0 * 3 + i]) && signbit(x[1 * 3 + i]) && signbit(x[2 * 3 + i]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            T v;
+            if (i == a && j == b) v = x[a * 3 + a] + x[b * 3 + b];
+            else if (j == b) v = x[i * 3 + a];
+            else if (i == a) v = x[b * 3 + j];
+            else v = (rneg[i] && cneg[j]) ? -T(0) : T(0);
+            put((i * 3 + j) + (a * 3 + b) * 9, v);
+          }
+    return true;
+  }
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
     for (int i = 0; i < 3; ++i)

@@ -151,12 +151,13 @@ NLK_FD void jac_sweeps(const T* u, const T* p, T* memo, JS J, bool& vals_ok, int
 
 // KM > 0: memo holds the KM transcendental values of F(u) (replayed)
 // Problems with an exact closed form of their dual-sweep Jacobian
-// (P::jac_closed_form, fed by the memo of F(u)) skip the sweeps when it
-// applies; it must return the sweeps' bits or decline (return false).
+// (P::jac_closed_form(u, memo, put)) skip the sweeps when it applies: it
+// must produce the sweeps' bits, entry by entry (put(e, v), column-major e),
+// or decline (return false, nothing put) -- then the sweeps run.
 template <class P, class = void> struct HasJacClosedForm { static constexpr bool value = false; };
 template <class P>
-struct HasJacClosedForm<P, std::void_t<decltype(&P::template jac_closed_form<double>)>> {
-  static constexpr bool value = true;
+struct HasJacClosedForm<P, std::void_t<decltype(P::kJacClosedForm)>> {
+  static constexpr bool value = P::kJacClosedForm;
 };
 #ifndef NLK_JAC_CLOSED_FORM
 #define NLK_JAC_CLOSED_FORM 1
@@ -164,13 +165,8 @@ struct HasJacClosedForm<P, std::void_t<decltype(&P::template jac_closed_form<dou
 
 template <class P, int N, class T, int KM, class JS>
 NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
-  if constexpr (NLK_JAC_CLOSED_FORM && KM > 0 && HasJacClosedForm<P>::value) {
-    T d[N], sv[N];
-    if (P::template jac_closed_form<T>(memo, d, sv)) {
-#pragma unroll
-      for (int e = 0; e < N * N; ++e) jput(J, e, (e % N == e / N) ? d[e % N] : sv[e / N]);
-      return -1;
-    }
+  if constexpr (NLK_JAC_CLOSED_FORM && HasJacClosedForm<P>::value && std::is_same<T, double>::value) {
+    if (P::jac_closed_form(u, memo, [&](int e, T v) { jput(J, e, v); })) return -1;
   }
   bool vals_ok = true;
   int bad_col = N;

@@ -99,3 +99,27 @@ def test_trig_zero_components_match_oracle():
         for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
             assert np.array_equal(got[f], ref[f]), (alg, f)
         assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
+
+
+def test_matrix_sqrt_sign_patterns_match_oracle():
+    """matrix-sqrt-3x3's closed-form Jacobian: all-negative rows/columns of X
+    (structural zeros become -0), exact zeros (declined: dual sweeps), every
+    algorithm that forms a Jacobian, bit-identical to the oracle."""
+    rng = np.random.default_rng(6)
+    B = 4096
+    u0 = rng.uniform(0.05, 2.0, (B, 9)) * rng.choice([-1.0, 1.0], (B, 9))
+    X = u0.reshape(B, 3, 3)
+    for i in range(B):
+        if i % 3 == 0:
+            X[i, i % 9 // 3, :] = -np.abs(X[i, i % 9 // 3, :])  # a negative row
+        if i % 5 == 0:
+            X[i, :, i % 7 % 3] = -np.abs(X[i, :, i % 7 % 3])  # a negative column
+        if i % 11 == 0:
+            X[i].flat[rng.integers(9)] = rng.choice([0.0, -0.0])
+    u0 = X.reshape(B, 9)
+    for alg in ("trust-region", "newton-raphson", "newton-backtracking"):
+        got = _solve("test23/matrix-sqrt-3x3", alg, u0, None, 1e-8, 1000)
+        ref = O.solve_batch("test23/matrix-sqrt-3x3", alg, u0, None)
+        for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+            assert np.array_equal(got[f], ref[f]), (alg, f)
+        assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
