@@ -424,8 +424,58 @@ struct BroydenBanded {  // 201-210
     }
   }
 };
+// The dual sweep's Jacobian of R = X @ X - A (object matmul, X = D x D,
+// row-major) in closed form.  Entry (row i*D+j, column a*D+b) of the sweep is
+// sum_l (X_il*[l==a][j==b] + X_lj*[i==a][l==b]) with every product formed
+// (v*1 or v*0) and summed over l in order.  With every X entry nonzero the
+// nonzero terms are exact and the zeros cannot change them: j==b, i!=a ->
+// X_ia; i==a, j!=b -> X_bj; i==a, j==b -> X_aa + X_bb (a == b: X_aa + X_aa);
+// otherwise all 2D products are zeros carrying the signs of X_il and X_lj, and
+// the sum is -0 iff row i and column j of X are all negative.  Declines (the
+// sweeps run) when an entry is zero, or large enough for the sweep's value
+// path to overflow where the float path did not.
+template <int D, class T, class PUT>
+NLK_FD bool matsq_jac_closed_form(const T* x, PUT&& put) {
+  bool ok = true;
+#pragma unroll
+  for (int e = 0; e < D * D; ++e) ok &= (x[e] != T(0)) && (fabs(x[e]) < T(1e150));
+  if (!ok) return false;
+  bool rneg[D], cneg[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    rneg[i] = cneg[i] = true;
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      rneg[i] = rneg[i] && signbit(x[i * D + l]);
+      cneg[i] = cneg[i] && signbit(x[l * D + i]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          T v;
+          if (i == a && j == b) v = x[a * D + a] + x[b * D + b];
+          else if (j == b) v = x[i * D + a];
+          else if (i == a) v = x[b * D + j];
+          else v = (rneg[i] && cneg[j]) ? -T(0) : T(0);
+          put((i * D + j) + (a * D + b) * D * D, v);
+        }
+  return true;
+}
 struct MatrixSqrt2x2 {  // 213-220
   static constexpr int N = 4, M = 0;
+  // out[i*2+j] = X_i0 X_0j + X_i1 X_1j (- A_ij): the object matmul of
+  // matsq_jac_closed_form, written out
+  static constexpr bool kJacClosedForm = true;
+  template <class T, class PUT>
+  NLK_FD static bool jac_closed_form(const T* x, const T*, PUT&& put) {
+    return matsq_jac_closed_form<2>(x, put);
+  }
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] * x[0] + x[1] * x[2] - K(1e-4);
     out[1] = x[0] * x[1] + x[1] * x[3] - K(1.0);
@@ -435,45 +485,11 @@ struct MatrixSqrt2x2 {  // 213-220
 };
 struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
   static constexpr int N = 9, M = 0;
-  // The dual sweep's Jacobian in closed form.  Entry (row i*3+j, column
-  // a*3+b) of the object matmul's sweep is sum_l (X_il*[l==a][j==b] +
-  // X_lj*[i==a][l==b]) with every product formed (v*1 or v*0) and summed over
-  // l in order.  With every X entry nonzero the nonzero terms are exact and
-  // the zeros cannot change them: j==b, i!=a -> X_ia; i==a, j!=b -> X_bj;
-  // i==a, j==b -> X_aa + X_bb (a == b: X_aa + X_aa); otherwise all six
-  // products are zeros carrying the signs of X_il and X_lj, and the sum is
-  // -0 iff row i and column j of X are all negative.  Declines (sweeps run)
-  // when an entry is zero, or large enough for the sweep's value path to
-  // overflow where the float path did not.
+  // closed-form Jacobian: matsq_jac_closed_form (above)
   static constexpr bool kJacClosedForm = true;
   template <class T, class PUT>
   NLK_FD static bool jac_closed_form(const T* x, const T*, PUT&& put) {
-    bool ok = true;
-#pragma unroll
-    for (int e = 0; e < 9; ++e) ok &= (x[e] != T(0)) && (fabs(x[e]) < T(1e150));
-    if (!ok) return false;
-    bool rneg[3], cneg[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      rneg[i] = signbit(x[i * 3 + 0]) && signbit(x[i * 3 + 1]) && signbit(x[i * 3 + 2]);
-      cneg[i] = signbit(x[0 * 3 + i]) && signbit(x[1 * 3 + i]) && signbit(x[2 * 3 + i]);
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            T v;
-            if (i == a && j == b) v = x[a * 3 + a] + x[b * 3 + b];
-            else if (j == b) v = x[i * 3 + a];
-            else if (i == a) v = x[b * 3 + j];
-            else v = (rneg[i] && cneg[j]) ? -T(0) : T(0);
-            put((i * 3 + j) + (a * 3 + b) * 9, v);
-          }
-    return true;
+    return matsq_jac_closed_form<3>(x, put);
   }
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll

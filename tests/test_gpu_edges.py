@@ -101,25 +101,27 @@ def test_trig_zero_components_match_oracle():
         assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
 
 
-def test_matrix_sqrt_sign_patterns_match_oracle():
-    """matrix-sqrt-3x3's closed-form Jacobian: all-negative rows/columns of X
+@pytest.mark.parametrize("D", [2, 3])
+def test_matrix_sqrt_sign_patterns_match_oracle(D):
+    """matrix-sqrt-DxD's closed-form Jacobian: all-negative rows/columns of X
     (structural zeros become -0), exact zeros (declined: dual sweeps), every
     algorithm that forms a Jacobian, bit-identical to the oracle."""
-    rng = np.random.default_rng(6)
-    B = 4096
-    u0 = rng.uniform(0.05, 2.0, (B, 9)) * rng.choice([-1.0, 1.0], (B, 9))
-    X = u0.reshape(B, 3, 3)
+    rng = np.random.default_rng(6 + D)
+    B, n = 4096, D * D
+    pid = f"test23/matrix-sqrt-{D}x{D}"
+    u0 = rng.uniform(0.05, 2.0, (B, n)) * rng.choice([-1.0, 1.0], (B, n))
+    X = u0.reshape(B, D, D)
     for i in range(B):
         if i % 3 == 0:
-            X[i, i % 9 // 3, :] = -np.abs(X[i, i % 9 // 3, :])  # a negative row
+            X[i, i % D, :] = -np.abs(X[i, i % D, :])  # a negative row
         if i % 5 == 0:
-            X[i, :, i % 7 % 3] = -np.abs(X[i, :, i % 7 % 3])  # a negative column
+            X[i, :, (i // 5) % D] = -np.abs(X[i, :, (i // 5) % D])  # a negative column
         if i % 11 == 0:
-            X[i].flat[rng.integers(9)] = rng.choice([0.0, -0.0])
-    u0 = X.reshape(B, 9)
+            X[i].flat[rng.integers(n)] = rng.choice([0.0, -0.0])
+    u0 = X.reshape(B, n)
     for alg in ("trust-region", "newton-raphson", "newton-backtracking"):
-        got = _solve("test23/matrix-sqrt-3x3", alg, u0, None, 1e-8, 1000)
-        ref = O.solve_batch("test23/matrix-sqrt-3x3", alg, u0, None)
+        got = _solve(pid, alg, u0, None, 1e-8, 1000)
+        ref = O.solve_batch(pid, alg, u0, None)
         for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
             assert np.array_equal(got[f], ref[f]), (alg, f)
         assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
