@@ -125,3 +125,25 @@ def test_matrix_sqrt_sign_patterns_match_oracle(D):
         for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
             assert np.array_equal(got[f], ref[f]), (alg, f)
         assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
+
+
+def test_brown_almost_linear_closed_form_edges_match_oracle():
+    """brown-almost-linear's closed-form Jacobian: exact zeros, mixed signs,
+    components whose products underflow or grow large (declined where signed
+    zeros or overflow decide), bit-identical to the oracle."""
+    rng = np.random.default_rng(8)
+    B = 4096
+    u0 = rng.uniform(0.2, 1.5, (B, 10)) * rng.choice([-1.0, 1.0], (B, 10))
+    for i in range(B):
+        if i % 7 == 0:
+            u0[i, rng.integers(10)] = rng.choice([0.0, -0.0])
+        if i % 13 == 0:
+            u0[i, :5] *= 1e-70  # prefix products underflow
+        if i % 17 == 0:
+            u0[i, rng.integers(10)] = 1e40
+    for alg in ("newton-raphson", "trust-region", "newton-backtracking"):
+        got = _solve("test23/brown-almost-linear", alg, u0, None, 1e-8, 1000)
+        ref = O.solve_batch("test23/brown-almost-linear", alg, u0, None)
+        for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+            assert np.array_equal(got[f], ref[f]), (alg, f)
+        assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
