@@ -75,6 +75,18 @@ NLK_TRANS_ATTR SinCos nlk_sincos_v(double x) {
   glibc::sincos(x, &r.s, &r.c);
   return r;
 }
+// two arguments per out-of-line call, evaluated branch-free side by side
+// (glibc::sincos_n<2>; the rare Payne-Hanek / non-finite arguments take the
+// scalar port inside the call): NLK_SINCOS_PAIRS
+struct SinCos2 { double s0, c0, s1, c1; };
+NLK_TRANS_ATTR SinCos2 nlk_sincos2_v(double x0, double x1) {
+  double x[2] = {x0, x1}, sv[2], cv[2];
+  if (glibc::sincos_n<2>(x, sv, cv)) {
+    if (glibc::sincos_slow(x0)) glibc::sincos(x0, &sv[0], &cv[0]);
+    if (glibc::sincos_slow(x1)) glibc::sincos(x1, &sv[1], &cv[1]);
+  }
+  return SinCos2{sv[0], cv[0], sv[1], cv[1]};
+}
 __device__ __forceinline__ void nlk_sincos(double x, double* s, double* c) {
   const SinCos r = nlk_sincos_v(x);
   *s = r.s;

@@ -97,7 +97,12 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
 #ifndef NLK_SINCOS_GROUP
 #define NLK_SINCOS_GROUP 0
 #endif
-template <class T, int MODE>
+// 1: Newton-Raphson's residual evaluations take sincos in pairs per
+// out-of-line call (nlk_sincos2_v; Base<..., SCPAIRS>)
+#ifndef NLK_SINCOS_PAIRS_NR
+#define NLK_SINCOS_PAIRS_NR 1
+#endif
+template <class T, int MODE, bool SCPAIRS = false>
 struct Ctx {
   T* m;
   int i;
@@ -120,7 +125,18 @@ struct Ctx {
   // sincos of G arguments: the fp64 float path evaluates them together
   // (glibc::sincos_n, G-way ILP; same bits as G separate calls)
   template <int G, class S> NLK_FD void sincos_all(const S* x, S* s, S* c) {
-    if constexpr (std::is_same<S, double>::value && NLK_SINCOS_GROUP > 0) {
+    if constexpr (std::is_same<S, double>::value && SCPAIRS && G % 2 == 0) {
+#pragma unroll
+      for (int g = 0; g < G; g += 2) {
+        const SinCos2 r = nlk_sincos2_v(x[g], x[g + 1]);
+        s[g] = r.s0; c[g] = r.c0; s[g + 1] = r.s1; c[g + 1] = r.c1;
+      }
+      if constexpr (MODE == 1) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) { m[i + 2 * g] = s[g]; m[i + 2 * g + 1] = c[g]; }
+      }
+      i += 2 * G;
+    } else if constexpr (std::is_same<S, double>::value && NLK_SINCOS_GROUP > 0) {
       constexpr int GG = NLK_SINCOS_GROUP < G ? NLK_SINCOS_GROUP : G;
 #pragma unroll
       for (int g0 = 0; g0 < G; g0 += GG) {

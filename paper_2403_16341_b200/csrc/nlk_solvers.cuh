@@ -177,8 +177,11 @@ NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
 }
 
 // MEMO: record F's transcendentals for the next Jacobian (drivers that
-// never form a Jacobian -- quasi-Newton, DFSane -- pass false)
-template <class P, int N, class T, bool MEMO = true>
+// never form a Jacobian -- quasi-Newton, DFSane -- pass false).
+// SCPAIRS: residuals evaluate their sincos in pairs per out-of-line call
+// (Ctx::sincos_all; measured faster for Newton, slower for the trust region,
+// whose extra live state then spills)
+template <class P, int N, class T, bool MEMO = true, bool SCPAIRS = false>
 struct Base {
   static constexpr int M = P::M;
   T u[N], f[N];
@@ -192,7 +195,7 @@ struct Base {
 
   NLK_FD void F(const T* x, T* out) {  // CountedResidual.at (core.py:119-123)
     nf += 1;
-    Ctx<T, (KM > 0 ? 1 : 0)> cx{memo, 0};
+    Ctx<T, (KM > 0 ? 1 : 0), SCPAIRS> cx{memo, 0};
     P::template f<T, T>(x, p, out, cx);
   }
   // Precondition (memo): the last F call was at u.  Holds at every call site:
@@ -218,8 +221,8 @@ struct Base {
 
 // ---- Newton-Raphson (optionally with backtracking line search) --------------
 template <class P, int N, class T, bool LS>
-struct NewtonRaphson : Base<P, N, T> {
-  using B = Base<P, N, T>;
+struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
+  using B = Base<P, N, T, true, NLK_SINCOS_PAIRS_NR>;
   static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_NR_MIN>::value;
   static constexpr int kSmemElems = SM ? N * N + N : 0;
   NLK_FD int init(T abstol) { return B::start(abstol); }
