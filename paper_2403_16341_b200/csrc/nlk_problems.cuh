@@ -102,6 +102,9 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
 #ifndef NLK_SINCOS_PAIRS_NR
 #define NLK_SINCOS_PAIRS_NR 1
 #endif
+#ifndef NLK_SINCOS_PAIRS_TR
+#define NLK_SINCOS_PAIRS_TR 0
+#endif
 template <class T, int MODE, bool SCPAIRS = false>
 struct Ctx {
   T* m;
@@ -372,14 +375,20 @@ struct Trigonometric {  // 171-177
   // always finite.)
   static constexpr bool kJacClosedForm = true;
   template <class T, class PUT>
-  NLK_FD static bool jac_closed_form(const T*, const T* memo, PUT&& put) {
+  NLK_FD static bool jac_closed_form(const T* u, const T* memo, PUT&& put) {
+    T sc[2 * N];  // without a memo: glibc sin/cos of u, as F(u) computed them
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (memo) { sc[2 * j] = memo[2 * j]; sc[2 * j + 1] = memo[2 * j + 1]; }
+      else t_sincos(u[j], sc[2 * j], sc[2 * j + 1]);
+    }
     bool ok = true;
 #pragma unroll
-    for (int j = 0; j < N; ++j) ok &= (memo[2 * j] != T(0));
+    for (int j = 0; j < N; ++j) ok &= (sc[2 * j] != T(0));
     if (!ok) return false;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      const T sj = memo[2 * j], cj = memo[2 * j + 1];
+      const T sj = sc[2 * j], cj = sc[2 * j + 1];
       const T dj = (sj + T(j + 1) * sj) - cj;
 #pragma unroll
       for (int i = 0; i < N; ++i) put(i + j * N, i == j ? dj : sj);

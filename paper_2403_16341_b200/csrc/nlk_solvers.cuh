@@ -166,7 +166,10 @@ struct HasJacClosedForm<P, std::void_t<decltype(P::kJacClosedForm)>> {
 template <class P, int N, class T, int KM, class JS>
 NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
   if constexpr (NLK_JAC_CLOSED_FORM && HasJacClosedForm<P>::value && std::is_same<T, double>::value) {
-    if (P::jac_closed_form(u, memo, [&](int e, T v) { jput(J, e, v); })) return -1;
+    // memo = nullptr: the driver keeps no memo (the closed form evaluates
+    // what it needs itself)
+    if (P::jac_closed_form(u, KM > 0 ? memo : nullptr, [&](int e, T v) { jput(J, e, v); }))
+      return -1;
   }
   bool vals_ok = true;
   int bad_col = N;
@@ -303,8 +306,8 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 #define NLK_TR_DLCACHE 1
 #endif
 template <class P, int N, class T>
-struct TrustRegion : Base<P, N, T, NLK_TR_MEMO> {
-  using B = Base<P, N, T, NLK_TR_MEMO>;
+struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
+  using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR>;
   static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_TR_MIN>::value;
   // JSM: J also in shared memory (after LU and rhs) instead of registers
   static constexpr bool JSM =
