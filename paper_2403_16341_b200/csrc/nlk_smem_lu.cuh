@@ -15,6 +15,7 @@
 // sequence as nlk_blas.cuh, element for element.
 #pragma once
 #include "nlk_blas.cuh"
+#include "nlk_div.cuh"
 
 namespace nlk {
 
@@ -35,6 +36,10 @@ namespace nlk {
 #define NLK_SMU _Pragma("unroll 1")
 #endif
 
+// 1: getrs' back substitution divides with reciprocals refined up front
+#ifndef NLK_GETRS_HOIST_DIV
+#define NLK_GETRS_HOIST_DIV 0
+#endif
 // 1: getrs substitutes on a register copy of the permuted right-hand side
 #ifndef NLK_GETRS_REG
 #define NLK_GETRS_REG 0
@@ -400,9 +405,20 @@ NLK_SMU
 NLK_SMU
     for (int r = i + 1; r < N; ++r) b.v(r) = t_fma(-bi, LU(r, i), b.v(r));
   }
+#if NLK_GETRS_HOIST_DIV
+  // the divisors' reciprocal refinements first (independent), then each
+  // division of the serial chain finishes in three operations (nlk_div.cuh)
+  T rd[N];
+NLK_SMU
+  for (int i = 0; i < N; ++i) rd[i] = div_rcp(LU(i, i));
+#endif
 NLK_SMU
   for (int i = N - 1; i >= 0; --i) {
+#if NLK_GETRS_HOIST_DIV
+    const T bi = div_with_rcp(b.v(i), LU(i, i), rd[i]);
+#else
     const T bi = b.v(i) / LU(i, i);
+#endif
     b.v(i) = bi;
 NLK_SMU
     for (int r = 0; r < i; ++r) b.v(r) = t_fma(-bi, LU(r, i), b.v(r));
