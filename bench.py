@@ -365,7 +365,8 @@ def run_ours(args, rank, world, local_rank, dist):
             for st_ in e2e_streams:
                 st_.synchronize()
 
-        e2e_step()  # warm-up (allocations, first-touch)
+        for _ in range(2):  # warm-up (allocations, first-touch, clocks after the idle setup)
+            e2e_step()
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -434,7 +435,7 @@ def main():
                     help="default 1e-8 (f32 on the quadratics: 1e-6)")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
                     help="arithmetic type (f32: registered fp32 instances, C1/C3/C4/C5)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--streams", type=int, default=1,
                     help="device-resident step: jobs round-robin over this many streams")
     ap.add_argument("--cpu-sample", type=int, default=60, help="systems per job for the CPU leg")

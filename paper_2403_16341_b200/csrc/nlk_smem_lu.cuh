@@ -19,12 +19,16 @@
 
 namespace nlk {
 
-// n thresholds for the shared-memory path, per driver
+// n thresholds for the shared-memory path, per driver.  First used for
+// n >= 9 only; measured on the C2/C5 jobs (profiles/r01c_variants_ab.txt)
+// the shared-memory LU is as fast or faster down to n = 2 as well (n = 4
+// trust region: 34.5 -> 29.2 ms on matrix-sqrt-2x2; the register LU's
+// predicated interchanges disappear), so only n = 1 keeps registers.
 #ifndef NLK_SMEM_NR_MIN
-#define NLK_SMEM_NR_MIN 9
+#define NLK_SMEM_NR_MIN 2
 #endif
 #ifndef NLK_SMEM_TR_MIN
-#define NLK_SMEM_TR_MIN 9
+#define NLK_SMEM_TR_MIN 2
 #endif
 // 1: unroll every loop (immediate smem offsets); 0: rolled loops
 #ifndef NLK_SMEM_UNROLL

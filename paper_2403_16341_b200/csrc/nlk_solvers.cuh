@@ -406,9 +406,10 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   // 2 + gg, t_star, |cauchy|; 3 g in the rhs slot instead -- set once the
   // scaled-gradient branch is taken: the radius only shrinks until the next
   // accepted step, so the Newton step and the segment are not needed again.
-  // Measured (C2 jobs, B = 2^20): trigonometric 326 -> 283 ms; for the
-  // register path (n < 9) the extra loop-carried state cost more than it
-  // saved (matrix-sqrt-2x2 36 -> 47 ms), so it keeps dogleg_plain.
+  // Measured (C2 jobs, B = 2^20): trigonometric 326 -> 283 ms; on the
+  // register-LU path the extra loop-carried state cost more than it saved
+  // (matrix-sqrt-2x2 with a register LU: 36 -> 47 ms), so it keeps
+  // dogleg_plain.
   static constexpr bool kDlCache = SM && NLK_TR_DLCACHE;
   T nnorm, gg, t_star, cnorm;
   int dl;
