@@ -32,6 +32,16 @@ template <int N, class T> NLK_FD bool all_finite(const T* x) {
   for (int i = 0; i < N; ++i) ok &= isfinite(x[i]);
   return ok;
 }
+// bitwise equality of two vectors (distinguishes -0/+0, NaN payloads)
+template <int N, class T> NLK_FD bool same_bits(const T* a, const T* b) {
+  bool eq = true;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    if constexpr (sizeof(T) == 8) eq &= (__double_as_longlong(a[i]) == __double_as_longlong(b[i]));
+    else eq &= (__float_as_int(a[i]) == __float_as_int(b[i]));
+  }
+  return eq;
+}
 // np.max(np.abs(x)) with NaN propagation
 template <int N, class T> NLK_FD T max_abs(const T* x) {
   T m = fabs(x[0]);
@@ -305,6 +315,10 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 #ifndef NLK_TR_DLCACHE
 #define NLK_TR_DLCACHE 1
 #endif
+// fast-forward a radius-exhaustion tail of bit-identical rejections (step())
+#ifndef NLK_TR_FASTFWD
+#define NLK_TR_FASTFWD 1
+#endif
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR>;
@@ -536,6 +550,31 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
       B::nsteps += 1;
       cached = false;
       if (converged<N>(B::f, abstol)) return SUCCESS;
+    }
+    if constexpr (kDlCache && NLK_TR_FASTFWD) {
+      // Radius-exhaustion fast-forward.  A rejection in the scaled-gradient
+      // branch (dl == 3) whose trial point rounds back to u bit for bit
+      // (and re-evaluates to the same f) fixes every remaining iteration:
+      // the next radii only shrink, so each later step s'*g has
+      // |s'| <= |s| with the same sign and, rounding being monotone,
+      // u + s'*g == u again; F(u) == f, so actual reduction is exactly 0 and
+      // rho is 0, -inf or NaN -- a rejection every time (globalize.py:
+      // 196-212).  What remains of those iterations is the counters and the
+      // radius halving, replayed here with the same operations.  Measured on
+      // test23/trigonometric TR: the MaxIters tail is ~85 % such iterations.
+      if (!accept && dl == 3 && same_bits<N>(ut, B::u) && same_bits<N>(ft, B::f)) {
+        int k = B::k, extra = 0;
+        while (!(radius < Num<T>::radius_stop) && k < maxiters) {
+          k += 1;
+          extra += 1;
+          T sh = T(0.5) * radius;
+          radius = (Num<T>::radius_floor > sh) ? Num<T>::radius_floor : sh;
+        }
+        B::k = k;
+        B::nlinsolve += extra;
+        B::nf += extra;
+        return MAXITERS;
+      }
     }
     if (radius < Num<T>::radius_stop) return MAXITERS;
     return B::k >= maxiters ? MAXITERS : RUNNING;
