@@ -180,3 +180,22 @@ def test_drop_in_single_solve_and_polyalgorithm():
     g = nlk.get_problem("generalized_rosenbrock?N=8")
     r = nlk.run_preset("klement", g.problem)
     assert r.retcode is nlk.RetCode.NONFINITE and r.stats.nsteps == 12
+
+
+@pytest.mark.parametrize("maxiters", [150, 400, 1000, 3000])
+@pytest.mark.parametrize("index,sigma", [(11, 0.1), (11, 1.0), (16, 1.0), (17, 1.0), (21, 1.0), (8, 1.0), (15, 1.0), (4, 1.0)])
+def test_trust_region_fast_forward(index, sigma, maxiters):
+    """The trust region's radius-exhaustion fast-forward (nlk_solvers.cuh,
+    TrustRegion::step) replays the counters and the radius halving of a tail
+    of bit-identical rejections.  Both ways out of that tail are exercised:
+    maxiters (150..1000) and the radius underflow break (globalize.py:211-212,
+    reached before maxiters = 3000 by the trigonometric, dennis-schnabel and
+    freudenstein-roth MaxIters runs)."""
+    from oracle import oracle as O
+    b = W.c2_suite(index, 20000, 24000, sigma)
+    ref = O.solve_batch(b.problem_id, "trust-region", b.u0, maxiters=maxiters)
+    got = gpu_solve(b.problem_id, "trust-region", b.u0, maxiters=maxiters)
+    check_against(ref, got, f"C2 #{index} TR sigma={sigma} maxiters={maxiters}", b.problem_id)
+    if index in (11, 17, 21) and maxiters == 3000:
+        early = (got["retcode"] == 1) & (got["nlinsolve"] < maxiters)
+        assert early.any(), "radius-underflow exit not exercised"
