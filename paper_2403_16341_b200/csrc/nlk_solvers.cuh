@@ -563,14 +563,27 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
       // radius halving, replayed here with the same operations.  Measured on
       // test23/trigonometric TR: the MaxIters tail is ~85 % such iterations.
       if (!accept && dl == 3 && same_bits<N>(ut, B::u) && same_bits<N>(ft, B::f)) {
-        int k = B::k, extra = 0;
-        while (!(radius < Num<T>::radius_stop) && k < maxiters) {
-          k += 1;
-          extra += 1;
-          T sh = T(0.5) * radius;
-          radius = (Num<T>::radius_floor > sh) ? Num<T>::radius_floor : sh;
+        // The loop `while (!(radius < stop) && k < maxiters) { k++; radius =
+        // max(floor, radius / 2); }` in closed form: from radius >= stop the
+        // halvings are exact and stay above floor until the radius drops
+        // below stop, so the trip count is min(m, maxiters - k) with m the
+        // number of halvings that takes the radius below stop (found from
+        // the exponents, checked with exact ldexp).  An infinite radius never
+        // drops.  Only the trip count is observable (the radius is not
+        // returned).
+        const int left = maxiters - B::k;
+        int m;
+        if (radius < Num<T>::radius_stop) {
+          m = 0;
+        } else if (!isfinite(radius)) {
+          m = left;
+        } else {
+          m = ilogb(radius) - ilogb(Num<T>::radius_stop) - 1;
+          if (m < 0) m = 0;
+          while (!(ldexp(radius, -m) < Num<T>::radius_stop)) ++m;
         }
-        B::k = k;
+        const int extra = (left <= 0) ? 0 : (m < left ? m : left);
+        B::k += extra;
         B::nlinsolve += extra;
         B::nf += extra;
         return MAXITERS;
