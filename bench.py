@@ -2,7 +2,7 @@
 """Throughput benchmark of the batched Simple* solvers (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c1|c3|c4|c5] [--batch B]
+                    [--config c2|c1|c3|c4|c5] [--batch B | --global-batch G]
 
 One *step* = one pass of the hot path over one batch: for the default
 workload (config C2, the configuration the metric is quoted on for one B200)
@@ -10,21 +10,32 @@ that is every one of the 23 MINPACK / More-Garbow-Hillstrom problems at B
 perturbed initial guesses (u0 = u0c + 0.1*max(1,|u0c|_inf)*U(-1,1)^n) solved
 with SimpleNewtonRaphson and with SimpleTrustRegion: 46 kernel launches,
 23*2*B systems.  With N GPUs (torchrun, one process per GPU) every rank
-solves its own contiguous shard of an N*B global batch (weak scaling, no
-inter-GPU traffic in the solve); time is the max over ranks.
+solves its own contiguous shard: of an N*B batch per job (--batch, weak
+scaling) or of a fixed G per job (--global-batch, strong scaling, e.g. C4's
+10 M over 2/4/8 GPUs).  No inter-GPU traffic in the solve; time is the max
+over ranks.
 
 Reported on one JSON line (rank 0):
   value    systems solved/s, inputs resident in HBM, CUDA events on the
            launching stream, barrier + synchronize on both sides;
   e2e      same metric through the C-ABI with HOST buffers
            (nlk_solve_batch_host_async per job on 6 streams: pinned H2D,
-           solve, D2H of every output inside the timing);
-  roofline dominant kernel: algorithmic FP64 FLOPs (SURVEY.md §8d,
-           paper_2403_16341_b200/flops.py) / its CUDA-event duration, against
-           the FP64 FMA peak measured on this GPU by nlk_fp64_peak;
+           solve, D2H of every output inside the timing), max over ranks;
+  roofline dominant kernel, bound chosen by its arithmetic intensity
+           (algorithmic FLOPs / algorithmic HBM bytes, SURVEY.md §8d,
+           paper_2403_16341_b200/flops.py) against the ridge point: FP64
+           FLOP/s against the FP64 FMA peak measured in this run by
+           nlk_fp64_peak, or HBM GB/s against MEASURED_PEAKS.json; both
+           fractions are always reported;
   cpu_baseline  the unmodified reference (nlkit, oracle/_ref) on the host
-           cores with a process pool, on a bounded sample of the same inputs.
-`--impl reference` times only the reference on the host cores.
+           cores with a process pool, on a stratified sample of >= 20k
+           systems of the same jobs (N = 1, rank 0);
+  parity   those reference outputs against this arm's outputs for the same
+           systems, bit for bit (u, resid, retcode, nsteps, nf, njac,
+           nlinsolve), with the host fingerprint the reference's bits depend
+           on (CPU, OpenBLAS core, glibc, numpy SIMD).
+`--impl reference` times only the reference on the host cores: each step a
+stratified sample (--cpu-sample systems per job) of the same workload.
 """
 
 from __future__ import annotations
@@ -51,33 +62,37 @@ ALG_ID = {"newton-raphson": 0, "trust-region": 1, "broyden": 2, "klement": 3, "d
 
 
 # ---------------------------------------------------------------- workloads
-def jobs_for(config, lo, hi):
-    """[(problem_id, n, alg, Batch)] for rows [lo, hi) of each stream."""
+def iter_job_groups(config, lo, hi):
+    """Yield, one input batch at a time, the [(problem_id, n, alg, Batch)]
+    jobs that share it, for rows [lo, hi) of each stream."""
     from paper_2403_16341_b200 import workloads as W
-    out = []
     if config == "c2":
         for idx in range(1, 24):
             b = W.c2_suite(idx, lo, hi, 0.1)
-            for alg in ("newton-raphson", "trust-region"):
-                out.append((b.problem_id, b.n, alg, b))
+            yield [(b.problem_id, b.n, alg, b) for alg in ("newton-raphson", "trust-region")]
     elif config == "c1":
-        out.append(("quadratic", 2, "newton-raphson", W.c1_quadratic(lo, hi)))
+        yield [("quadratic", 2, "newton-raphson", W.c1_quadratic(lo, hi))]
     elif config == "c3":
         for n in (8, 16):
             b = W.c3_rosenbrock(n, lo, hi)
-            for alg in ("broyden", "klement"):
-                out.append((b.problem_id, n, alg, b))
+            yield [(b.problem_id, n, alg, b) for alg in ("broyden", "klement")]
     elif config == "c4":
-        out.append(("test23/broyden-tridiagonal", 16, "dfsane", W.c4_tridiagonal(lo, hi)))
+        yield [("test23/broyden-tridiagonal", 16, "dfsane", W.c4_tridiagonal(lo, hi))]
     elif config == "c5":
         b = W.c5_quadratic(lo, hi)
         algs = W.c5_algorithms(lo, hi)
+        out = []
         for k, alg in enumerate(W.C5_ALGS):
             sel = np.nonzero(algs == k)[0]
             out.append(("quadratic", 4, alg, W.Batch("quadratic", 4, b.u0[sel], b.p[sel], lo)))
+        yield out
     else:
         raise SystemExit(f"unknown config {config}")
-    return out
+
+
+def jobs_for(config, lo, hi):
+    """[(problem_id, n, alg, Batch)] for rows [lo, hi) of each stream."""
+    return [j for g in iter_job_groups(config, lo, hi) for j in g]
 
 
 WORKLOAD = {
@@ -161,28 +176,79 @@ def _nlkit_residual(nlp, problem_id, n):
 
 
 def _ref_solve(args):
+    """One system through the unmodified reference's public preset entry
+    point (nlkit.solvers.run_preset, solvers.py:640-655).  Returns every
+    per-system output the GPU arm returns: (retcode index, u bytes, resid,
+    nsteps, nf, njac, nlinsolve)."""
     problem_id, n, alg, u0, p = args
     import nlkit
     from nlkit import problems as nlp
     fun = _nlkit_residual(nlp, problem_id, n)
     prob = nlkit.Problem(fun, u0, params=p if p is not None else np.zeros(0))
     with np.errstate(all="ignore"):
-        if alg == "dfsane":
+        if alg == "dfsane":  # no reference algorithm: builder-authored statement
             from oracle import dfsane_ref
             res = dfsane_ref.run_dfsane(prob, nlkit.SolveOptions(), nlkit)
         else:
             res = nlkit.solvers.run_preset(alg, prob, nlkit.SolveOptions())
-    return res.retcode.value
+    st = res.stats
+    return (list(nlkit.RetCode).index(res.retcode),
+            np.asarray(res.u_star, dtype=np.float64).tobytes(), float(res.resid_norm),
+            int(st.nsteps), int(st.nf), int(st.njac), int(st.nlinsolve))
 
 
-def cpu_reference_rate(jobs, per_job, cores=None):
-    """Time the unmodified reference (process pool, one solve per task) on the
-    first `per_job` systems of every job; falls back to the C++ oracle port."""
+def stratified_rows(Bj, k, offset=0):
+    """Systematic sample of k of Bj rows (every Bj/k-th, shifted by offset):
+    the heavy-tailed iteration counts of a job are sampled in proportion."""
+    k = max(1, min(k, Bj))
+    idx = (np.arange(k, dtype=np.int64) * Bj) // k + offset
+    return idx[idx < Bj]
+
+
+def host_fingerprint():
+    """What the reference's bits depend on: CPU, the
+    OpenBLAS kernel family numpy/scipy dispatch to (getrf/getrs/gemv/dot
+    orders), glibc (libm FMA ifunc variants) and numpy's SIMD dispatch
+    (SVML exp/arctan)."""
+    fp = {"cores": os.cpu_count()}
+    try:
+        info = {}
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k = k.strip()
+            if k in ("model name", "cpu family", "model", "stepping") and k not in info:
+                info[k] = v.strip()
+        fp["cpu"] = info
+    except OSError:
+        pass
+    try:
+        fp["glibc"] = os.confstr("CS_GNU_LIBC_VERSION")
+    except (ValueError, OSError):
+        pass
+    fp["numpy"] = np.__version__
+    try:
+        from numpy._core._multiarray_umath import __cpu_features__ as F
+        fp["numpy_simd"] = sorted(k for k, v in F.items() if v and k.startswith("AVX512"))
+    except ImportError:
+        pass
+    try:
+        import scipy
+        import scipy.linalg  # noqa: F401  (loads scipy's OpenBLAS)
+        import threadpoolctl
+        fp["scipy"] = scipy.__version__
+        fp["blas"] = [{"lib": os.path.basename(x.get("filepath", "")),
+                       "version": x.get("version"), "core": x.get("architecture")}
+                      for x in threadpoolctl.threadpool_info() if x.get("user_api") == "blas"]
+    except ImportError:
+        pass
+    return fp
+
+
+def cpu_reference_run(tasks, cores=None):
+    """Run the unmodified reference (oracle/_ref) on `tasks` in a fork pool
+    over the host cores, one run_preset per system; returns (outputs, seconds,
+    kind).  Without oracle/_ref the C++ port of the path stands in."""
     cores = cores or os.cpu_count() or 1
-    tasks = []
-    for pid, n, alg, b in jobs:
-        for i in range(min(per_job, len(b.u0))):
-            tasks.append((pid, n, alg, b.u0[i], None if b.p is None else b.p[i]))
     ref = _ref_path()
     if ref is not None:
         import multiprocessing as mp
@@ -192,21 +258,112 @@ def cpu_reference_rate(jobs, per_job, cores=None):
         with mp.get_context("fork").Pool(cores) as pool:
             pool.map(_ref_solve, tasks[: max(cores * 2, 16)], chunksize=1)  # warm-up
             t0 = time.perf_counter()
-            pool.map(_ref_solve, tasks, chunksize=4)
+            outs = pool.map(_ref_solve, tasks, chunksize=4)
             dt = time.perf_counter() - t0
-        kind = "reference"
-    else:
-        from oracle import oracle as O
-        t0 = time.perf_counter()
-        for pid, n, alg, b in jobs:
-            k = min(per_job, len(b.u0))
-            O.solve_batch(pid, alg, b.u0[:k], None if b.p is None else b.p[:k], threads=cores)
-        dt = time.perf_counter() - t0
-        kind = "port"
-    return {"value": len(tasks) / dt, "unit": "systems/s", "cores": cores, "kind": kind,
-            "sample": f"first {per_job} systems of each of {len(jobs)} (problem, algorithm) "
-                      f"jobs = {len(tasks)} solves, one Problem per system, fork pool",
-            "seconds": dt}
+        return outs, dt, "reference", cores
+    from oracle import oracle as O
+    outs = []
+    t0 = time.perf_counter()
+    for pid, n, alg, u0, p in tasks:
+        r = O.solve_batch(pid, alg, u0[None, :], None if p is None else p[None, :], threads=1)
+        outs.append((int(r["retcode"][0]), r["u"][0].tobytes(), float(r["resid"][0]),
+                     int(r["nsteps"][0]), int(r["nf"][0]), int(r["njac"][0]),
+                     int(r["nlinsolve"][0])))
+    return outs, time.perf_counter() - t0, "port", 1
+
+
+PARITY_FIELDS = ("retcode", "u", "resid", "nsteps", "nf", "njac", "nlinsolve")
+
+
+def cpu_baseline_and_parity(prepared, per_job, compare=True):
+    """The CPU leg of the GPU arm: the reference on a stratified sample of
+    every job (per_job systems each), timed, and compared bit for bit with
+    the GPU arm's outputs for the same systems (u and resid as bit patterns,
+    retcode and the four counters exactly)."""
+    tasks, gpu = [], []
+    for pid, n, m, alg, h, u0, p, out, b in prepared:
+        Bj = int(u0.shape[1])
+        idx = stratified_rows(Bj, per_job)
+        it = torch_index(idx, out["u"].device)
+        gu = out["u"][:, it].t().contiguous().cpu().numpy()
+        gr = out["resid"][it].cpu().numpy()
+        grc = out["retcode"][it].cpu().numpy()
+        gc = out["counters"][:, it].cpu().numpy()
+        for j, i in enumerate(idx):
+            tasks.append((pid, n, alg, b.u0[i], None if b.p is None else b.p[i]))
+            gpu.append((int(grc[j]), gu[j].astype(np.float64).tobytes(),
+                        float(gr[j]), int(gc[0, j]), int(gc[1, j]), int(gc[2, j]),
+                        int(gc[3, j]), pid, alg, int(i)))
+    outs, dt, kind, cores = cpu_reference_run(tasks)
+    cb = {"value": len(tasks) / dt, "unit": "systems/s", "cores": cores, "kind": kind,
+          "sample": f"stratified: every (B/{per_job})-th system of each of {len(prepared)} "
+                    f"(problem, algorithm) jobs = {len(tasks)} solves, one run_preset per "
+                    f"system, fork pool over {cores} host cores",
+          "seconds": dt}
+    if not compare:
+        return cb, {"skipped": "fp32 arm: the reference computes in fp64 (fp32 is checked "
+                               "against the fp64 oracle at 1e-4 in tests/test_gpu_fp32.py)"}
+    by_field = {f: 0 for f in PARITY_FIELDS}
+    mism, examples = 0, []
+    pinned = unpinned = 0
+    for g, r in zip(gpu, outs):
+        bad = [f for k, f in enumerate(PARITY_FIELDS)
+               if (g[k] != r[k] if f != "resid" else
+                   np.float64(g[k]).tobytes() != np.float64(r[k]).tobytes())]
+        if g[8] == "dfsane":
+            unpinned += 1
+        else:
+            pinned += 1
+        if bad:
+            mism += 1
+            for f in bad:
+                by_field[f] += 1
+            if len(examples) < 8:
+                examples.append({"problem": g[7], "alg": g[8], "index": g[9], "fields": bad})
+    parity = {"systems": len(tasks), "mismatches": mism, "fields": list(PARITY_FIELDS),
+              "mismatches_by_field": by_field, "examples": examples,
+              "against": kind + (" (nlkit, unmodified)" if kind == "reference" else ""),
+              "systems_unpinned_dfsane": unpinned, "host": host_fingerprint()}
+    return cb, parity
+
+
+def torch_index(idx, device):
+    import torch
+    return torch.from_numpy(np.asarray(idx, dtype=np.int64)).to(device)
+
+
+def reference_arm_samples(config, B, per_job, steps):
+    """For each of `steps` steps, the (problem, algorithm) jobs of `config`
+    at batch B per job, each reduced to a stratified sample of per_job
+    systems shifted by one row per step (the steps cover different systems
+    of the same workload).  Batches are generated one at a time."""
+    from paper_2403_16341_b200 import workloads as W
+    out = [[] for _ in range(steps)]
+    for group in iter_job_groups(config, 0, B):
+        for pid, n, alg, b in group:
+            for s in range(steps):
+                idx = stratified_rows(len(b.u0), per_job, s)
+                out[s].append((pid, n, alg, W.Batch(b.problem_id, b.n, b.u0[idx].copy(),
+                                                    None if b.p is None else b.p[idx].copy(), 0)))
+        del group
+    return out
+
+
+def tasks_of(jobs):
+    return [(pid, n, alg, b.u0[i], None if b.p is None else b.p[i])
+            for pid, n, alg, b in jobs for i in range(len(b.u0))]
+
+
+def _hbm_peak():
+    """HBM GB/s denominator: the driver-measured copy bandwidth of this pool
+    (MEASURED_PEAKS.json), else the profiling recipe's stated fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return float(json.load(open(p))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+        except (KeyError, ValueError):
+            pass
+    return 6650.0, "of fallback (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -217,8 +374,12 @@ def run_ours(args, rank, world, local_rank, dist):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     L = _lib.lib()
-    B = args.batch
-    lo, hi = rank * B, (rank + 1) * B
+    if args.global_batch:  # strong scaling: a fixed batch per job split N ways
+        from paper_2403_16341_b200.workloads import shard_bounds
+        lo, hi = shard_bounds(args.global_batch, world, rank)
+    else:  # weak scaling: B per job per GPU, rank r takes rows [rB, (r+1)B)
+        lo, hi = rank * args.batch, (rank + 1) * args.batch
+    B = hi - lo
     f32 = args.dtype == "f32"
     tdt = torch.float32 if f32 else torch.float64
     esz = 4 if f32 else 8
@@ -303,7 +464,12 @@ def run_ours(args, rank, world, local_rank, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())
     per_step_systems = sum(int(x[5].shape[1]) for x in prepared)
-    value = world * per_step_systems * args.steps / elapsed
+    total_systems = per_step_systems
+    if dist:
+        ts_ = torch.tensor([float(per_step_systems)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ts_, op=dist.ReduceOp.SUM)
+        total_systems = int(ts_.item())
+    value = total_systems * args.steps / elapsed
 
     # per-launch durations (mean over steps) and the dominant kernel's roofline
     launch_ms = [statistics.mean(ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(args.steps))
@@ -382,8 +548,9 @@ def run_ours(args, rank, world, local_rank, dist):
         bo = sum(x[5][0].numel() * esz + x[5][1].numel() * esz + x[5][2].numel() + x[5][3].numel() * 4
                  for x in host)
         # value: median step (robust to a one-off host hiccup); value_mean: all steps
-        e2e = {"value": world * per_step_systems / statistics.median(step_t),
-               "value_mean": world * per_step_systems * args.e2e_steps / float(te.item()),
+        # value: all steps, max over ranks; value_median: the median step (rank 0)
+        e2e = {"value": total_systems * args.e2e_steps / float(te.item()),
+               "value_median": total_systems / statistics.median(step_t),
                "unit": "systems/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "steps": args.e2e_steps, "step_ms": [round(1e3 * t, 1) for t in step_t],
                "streams": nst, "calls_per_step": len(host)}
@@ -397,29 +564,68 @@ def run_ours(args, rank, world, local_rank, dist):
         if t:
             traffic = t["dram_bytes"] * (prepared[jdom][5].shape[1] / t["batch"])
 
+    # The bound follows the dominant kernel's arithmetic intensity: algorithmic
+    # FLOPs per algorithmic HBM byte against the ridge point peak_flops /
+    # peak_bytes.  Below the ridge (the n = 2/4 quadratics) the kernel is
+    # HBM-bound and `achieved` is algorithmic GB/s; above it (every C2 job)
+    # the FP64 (FP32) pipe bounds it.  Both fractions are reported.
+    alg_bytes = flops.system_bytes(n, m, elem=esz) * prepared[jdom][5].shape[1]
+    hbm_peak, hbm_src = _hbm_peak()
+    ai = F / alg_bytes
+    ridge = fp64_peak * 1e12 / (hbm_peak * 1e9)
+    gbs = alg_bytes / dom_s / 1e9
+    pipe = "fp32" if f32 else "fp64"
+    hbm_bound = ai < ridge
+    ncu = None
+    npath = os.path.join(ROOT, "profiles", "ncu_pipe.json")
+    if os.path.exists(npath):
+        ncu = json.load(open(npath)).get(kernel_names[jdom])
+    roofline = {
+        "bound": "hbm" if hbm_bound else pipe,
+        "achieved": gbs if hbm_bound else achieved,
+        "peak": hbm_peak if hbm_bound else fp64_peak,
+        "unit": "GB/s" if hbm_bound else "TFLOP/s",
+        "frac": gbs / hbm_peak if hbm_bound else achieved / fp64_peak,
+        "traffic": traffic,
+        "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
+        "kernel": kernel_names[jdom], "launch_ms": launch_ms[jdom],
+        "flops_per_launch": F, "algorithmic_bytes": alg_bytes,
+        "arithmetic_intensity": ai, "ridge_flop_per_byte": ridge,
+        f"frac_{pipe}": achieved / fp64_peak, "frac_hbm": gbs / hbm_peak,
+        f"achieved_{pipe}_tflops": achieved, "achieved_hbm_gbs": gbs,
+        f"peak_{pipe}_tflops": fp64_peak,
+        f"peak_{pipe}_source": ("nlk_fp32_peak (FFMA chains" if f32 else "nlk_fp64_peak (DFMA chains")
+                               + ", measured in this run)",
+        "peak_hbm_gbs": hbm_peak, "peak_hbm_source": hbm_src,
+        "ncu": ncu,
+        "step_hbm_gbs": hbm_bytes / (elapsed / args.steps) / 1e9,
+    }
+
     result = {
         "metric": METRIC, "value": value, "unit": "systems/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "batch_per_job_per_gpu": B,
+                   "global_batch_per_job": args.global_batch or args.batch * world,
                    "jobs": len(prepared), "systems_per_step_per_gpu": per_step_systems,
                    "abstol": abstol, "maxiters": 1000,
                    "l2": f"inputs+outputs {hbm_bytes / 1e9:.2f} GB/step/GPU > 126 MB L2 (no flush needed)",
                    "parallelism": f"shard{world} (independent systems, no collective)"},
         "gpu_launches": len(prepared) * args.steps,
-        "roofline": {"bound": "fp32" if f32 else "fp64", "achieved": achieved, "peak": fp64_peak,
-                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
-                     "algorithmic_bytes": flops.system_bytes(n, m, elem=esz) * prepared[jdom][5].shape[1],
-                     "kernel": kernel_names[jdom], "launch_ms": launch_ms[jdom],
-                     "flops_per_launch": F,
-                     "peak_source": ("nlk_fp32_peak (FFMA chains" if f32 else "nlk_fp64_peak (DFMA chains")
-                                    + ", measured in this run)",
-                     "hbm_gbs": hbm_bytes / (elapsed / args.steps) / 1e9},
+        "roofline": roofline,
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    # CPU leg (rank 0, N = 1): the unmodified reference on a stratified sample
+    # of every job, timed, and compared bit for bit with this arm's outputs
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        per_job = max(1, -(-args.parity_systems // len(prepared)))
+        cb, parity = cpu_baseline_and_parity(prepared, per_job, compare=not f32)
+        cb.pop("seconds", None)
+        result["cpu_baseline"] = cb
+        result["parity"] = parity
     return result, stats, jobs
 
 
@@ -438,7 +644,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--streams", type=int, default=1,
                     help="device-resident step: jobs round-robin over this many streams")
-    ap.add_argument("--cpu-sample", type=int, default=60, help="systems per job for the CPU leg")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling: systems per job over ALL GPUs, split evenly "
+                         "(default: --batch per job per GPU, weak scaling)")
+    ap.add_argument("--parity-systems", type=int, default=20000,
+                    help="GPU arm: reference systems (stratified over the jobs) timed on the "
+                         "host and compared bit for bit with the GPU outputs")
+    ap.add_argument("--cpu-sample", type=int, default=60,
+                    help="reference arm: stratified systems per job per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats", default=None, help="write per-launch stats JSON here")
     ap.add_argument("--only", default=None,
@@ -453,22 +666,29 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        jobs = jobs_for(args.config, 0, max(args.cpu_sample, 1))
+        steps = args.warmup + args.steps
+        B = args.global_batch or args.batch
+        samples = reference_arm_samples(args.config, B, args.cpu_sample, steps)
         rates = []
-        for s in range(args.warmup + args.steps):
-            r = cpu_reference_rate(jobs, args.cpu_sample)
+        for s in range(steps):
+            tasks = tasks_of(samples[s])
+            _outs, dt, kind, cores = cpu_reference_run(tasks)
             if s >= args.warmup:
-                rates.append(r)
-        v = statistics.median(x["value"] for x in rates)
+                rates.append((len(tasks) / dt, dt, len(tasks)))
+        v = statistics.median(x[0] for x in rates)
+        sample = (f"stratified: {args.cpu_sample} systems (every B/{args.cpu_sample}-th, shifted "
+                  f"one row per step) of each of {len(samples[0])} (problem, algorithm) jobs at "
+                  f"B = {B} = {rates[0][2]} solves per step, one run_preset per system, fork pool")
         line = {"metric": METRIC, "value": v, "unit": "systems/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * statistics.median(x["seconds"] for x in rates),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": {"workload": WORKLOAD[args.config], "abstol": 1e-8, "maxiters": 1000,
-                           "parallelism": "host process pool"},
-                "cpu_baseline": {k: rates[0][k] for k in ("kind", "cores", "sample")} | {"value": v,
-                                                                                       "unit": "systems/s"},
+                "ms_per_step": 1e3 * statistics.median(x[1] for x in rates),
+                "higher_is_better": True, "scaling": "strong" if args.global_batch else "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": WORKLOAD[args.config], "batch_per_job": B,
+                           "abstol": 1e-8, "maxiters": 1000,
+                           "parallelism": f"host process pool ({cores} processes)"},
+                "cpu_baseline": {"kind": kind, "cores": cores, "sample": sample, "value": v,
+                                 "unit": "systems/s", "host": host_fingerprint()},
                 "e2e": {"value": v, "unit": "systems/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -483,10 +703,6 @@ def main():
         dist = tdist
     result, stats, jobs = run_ours(args, rank, world, local_rank, dist)
     if rank == 0:
-        if not args.no_cpu_baseline and world == 1:
-            cb = cpu_reference_rate(jobs, args.cpu_sample)
-            cb.pop("seconds", None)
-            result["cpu_baseline"] = cb
         if args.stats:
             with open(args.stats, "w") as fh:
                 json.dump({"result": result, "stats": stats}, fh, indent=1)
