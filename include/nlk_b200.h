@@ -13,6 +13,9 @@
  * Conventions
  *   - plain pointers and sizes only; no torch or CUDA types cross the boundary
  *     (streams are passed as void*; NULL = the legacy default stream);
+ *   - a call with a stream runs on that stream's device (the current device
+ *     is switched for the call and restored); with the NULL stream it runs
+ *     on the current device;
  *   - batch arrays are structure-of-arrays: u0/u_out are [n][B] (element i of
  *     system b at i*B + b), p is [m][B];
  *   - dtype 0 = IEEE binary64 (the reference's arithmetic), 1 = binary32;
@@ -62,6 +65,13 @@ extern "C" {
 /* Library version (major*10000 + minor*100 + patch). */
 NLK_API int nlk_version(void);
 
+/* Hash of the sources the library was built from (csrc/, include/):
+ * the first 16 hex digits of the SHA-256 over the sorted file names and
+ * contents, computed by paper_2403_16341_b200/build.py at build time.
+ * _lib.source_build_id() recomputes it from a source tree, so a caller can
+ * prove that the loaded binary is the one its sources describe. */
+NLK_API const char* nlk_build_id(void);
+
 /* Message of the last failed call on this thread ("" if none). */
 NLK_API const char* nlk_last_error(void);
 
@@ -90,6 +100,25 @@ NLK_API int nlk_solve_batch(int32_t handle, int32_t alg, int32_t dtype, int64_t 
                     const void* u0_soa, const void* p_soa, double abstol, int32_t maxiters,
                     void* u_out, void* resid_out, int8_t* retcode_out, int32_t* nsteps_out,
                     int32_t* nf_out, int32_t* njac_out, int32_t* nlinsolve_out, void* stream);
+
+/* The default poly-algorithm for a batch: replaces B calls of
+ * nlkit.solve(Problem(...)) / run_polyalgorithm(problem, options)
+ * (core.py:158-169, solvers.py:570-599).  Every registered problem has
+ * n <= QN_SKIP_THRESHOLD = 25, so the quasi-Newton stages are skipped and
+ * the stages are newton-raphson -> newton-backtracking -> trust-region
+ * (solvers.py:553-565), each with the full iteration budget.  A stage runs
+ * only on the systems no earlier stage solved; outputs are the first
+ * success, else the stage result with the smallest residual max-norm (the
+ * earliest on ties); the four counters are summed over the stages that ran.
+ * stage_retcodes_out is int8 [3][B]: the RetCode of stage s for system b at
+ * s*B + b, -1 where the stage did not run (SolveResult.stage_retcodes).
+ * Device buffers, asynchronous on `stream` (three launches, no host sync). */
+NLK_API int nlk_solve_batch_poly(int32_t handle, int32_t dtype, int64_t B, const void* u0_soa,
+                                 const void* p_soa, double abstol, int32_t maxiters,
+                                 void* u_out, void* resid_out, int8_t* retcode_out,
+                                 int32_t* nsteps_out, int32_t* nf_out, int32_t* njac_out,
+                                 int32_t* nlinsolve_out, int8_t* stage_retcodes_out,
+                                 void* stream);
 
 /* Same contract with HOST buffers (pageable or pinned): the library stages
  * the batch through device memory in chunks, overlapping host<->device copies

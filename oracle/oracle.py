@@ -193,3 +193,40 @@ def ift(problem_id, u, theta, gbar=None, abstol=1e-8):
     y = np.empty(n)
     lib().oracle_gemv_AT_x(n, np.ascontiguousarray(Ju), lam, y)
     return 0, -g, float(np.max(np.abs(y - gbar)))
+
+
+# ---- default poly-algorithm (solvers.py:570-599), restated -------------------
+POLY_STAGES = ("newton-raphson", "newton-backtracking", "trust-region")
+
+
+def poly_batch(problem_id, u0, p=None, abstol=1e-8, maxiters=1000, threads=None):
+    """run_polyalgorithm for n <= QN_SKIP_THRESHOLD (solvers.py:553-599): the
+    stages NR -> NR + backtracking -> TR, each run only while no earlier
+    stage succeeded; counters summed over the stages that ran; the result is
+    min(results, key=(not success, resid_norm)) -- Python's min keeps the
+    first of equal keys and never replaces on a NaN comparison.  Adds
+    ``stage_retcodes`` int8 [B, 3] (-1 = stage not run)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    B = u0.shape[0]
+    res = [solve_batch(problem_id, POLY_STAGES[0], u0, p, abstol, maxiters, threads)]
+    for stage in POLY_STAGES[1:]:
+        res.append(solve_batch(problem_id, stage, u0, p, abstol, maxiters, threads))
+    out = {k: v.copy() for k, v in res[0].items()}
+    out["stage_retcodes"] = np.full((B, 3), -1, np.int8)
+    for b in range(B):
+        best = 0
+        for s in range(3):
+            r = res[s]
+            out["stage_retcodes"][b, s] = r["retcode"][b]
+            if s > 0:
+                for k in ("nsteps", "nf", "njac", "nlinsolve"):
+                    out[k][b] += r[k][b]
+                key_new = (r["retcode"][b] != 0, r["resid"][b])
+                key_old = (res[best]["retcode"][b] != 0, res[best]["resid"][b])
+                if key_new < key_old:
+                    best = s
+            if r["retcode"][b] == 0:
+                break
+        for k in ("u", "resid", "retcode"):
+            out[k][b] = res[best][k][b]
+    return out

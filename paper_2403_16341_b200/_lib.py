@@ -26,9 +26,9 @@ ERRORS = {
 }
 
 # exported symbols, exactly those declared in include/nlk_b200.h
-SYMBOLS = ("nlk_version", "nlk_last_error", "nlk_alg_lookup", "nlk_num_problems",
+SYMBOLS = ("nlk_version", "nlk_build_id", "nlk_last_error", "nlk_alg_lookup", "nlk_num_problems",
            "nlk_problem_info", "nlk_problem_lookup", "nlk_solve_batch",
-           "nlk_solve_batch_host", "nlk_solve_batch_host_async", "nlk_last_grid",
+           "nlk_solve_batch_host", "nlk_solve_batch_host_async", "nlk_solve_batch_poly", "nlk_last_grid",
            "nlk_fp64_peak", "nlk_fp32_peak", "nlk_ift_forward_batch", "nlk_ift_adjoint_batch")
 
 _lib = None
@@ -52,6 +52,7 @@ def lib():
     pi32 = ctypes.POINTER(i32)
     L.nlk_version.restype = ctypes.c_int
     L.nlk_last_error.restype = ctypes.c_char_p
+    L.nlk_build_id.restype = ctypes.c_char_p
     L.nlk_alg_lookup.argtypes = [ctypes.c_char_p]
     L.nlk_num_problems.restype = ctypes.c_int
     L.nlk_problem_info.argtypes = [i32, ctypes.POINTER(ctypes.c_char_p), pi32, pi32]
@@ -62,6 +63,8 @@ def lib():
                                        vp, vp, vp, i64, i32]
     L.nlk_solve_batch_host_async.argtypes = [i32, i32, i32, i64, vp, vp, dbl, i32, vp, vp, vp,
                                              vp, vp, vp, vp, vp]
+    L.nlk_solve_batch_poly.argtypes = [i32, i32, i64, vp, vp, dbl, i32, vp, vp, vp, vp, vp, vp,
+                                       vp, vp, vp]
     L.nlk_last_grid.restype = ctypes.c_int
     L.nlk_fp64_peak.argtypes = [i64, ctypes.POINTER(dbl), vp]
     L.nlk_fp32_peak.argtypes = [i64, ctypes.POINTER(dbl), vp]
@@ -69,6 +72,17 @@ def lib():
     L.nlk_ift_adjoint_batch.argtypes = [i32, i32, i64, vp, vp, vp, dbl, vp, vp, vp, vp]
     _lib = L
     return L
+
+
+def build_id():
+    """nlk_build_id() of the loaded library."""
+    return lib().nlk_build_id().decode()
+
+
+def source_build_id():
+    """The build id of the sources in this tree (build.source_build_id)."""
+    from .build import source_build_id as sbi
+    return sbi()
 
 
 def check(rc):

@@ -62,6 +62,46 @@ def _compile(src, force, verbose, obj_dir=OBJ, defines=()):
     return obj, log
 
 
+def source_files():
+    """The files the library is built from (build-id inputs)."""
+    fs = []
+    for pat in ("*.cu", "*.cuh", "*.inc", "*.h"):
+        fs += glob.glob(os.path.join(CSRC, pat))
+    fs += glob.glob(os.path.join(INCLUDE, "*.h"))
+    return sorted(fs)
+
+
+def source_build_id():
+    """First 16 hex digits of SHA-256 over (relative name, contents) of every
+    source file, sorted by name (nlk_build_id() of a library built from them)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in source_files():
+        h.update(os.path.relpath(f, ROOT).encode() + b"\0")
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+        h.update(b"\0")
+    return h.hexdigest()[:16]
+
+
+def _build_id_object(obj_dir, defines):
+    """Compile the one-function TU that carries the build id (+ variant
+    defines, so a variant library reports what it was built with)."""
+    bid = source_build_id() + ("+" + ",".join(defines) if defines else "")
+    src = os.path.join(obj_dir, "nlk_build_id.cu")
+    obj = os.path.join(obj_dir, "nlk_build_id.o")
+    text = ('#include "nlk_b200.h"\n'
+            f'extern "C" NLK_API const char* nlk_build_id(void) {{ return "{bid}"; }}\n')
+    if not (os.path.exists(src) and open(src).read() == text and os.path.exists(obj)):
+        with open(src, "w") as fh:
+            fh.write(text)
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr[-4000:]}")
+    return obj
+
+
 def build(force=False, verbose=False, jobs=None, tag=None, defines=()):
     """Compile and link; ``tag``/``defines`` make a variant library
     ``libnlk_b200_<tag>.so`` (objects in ``_obj_<tag>``) for A/B timing."""
@@ -71,7 +111,7 @@ def build(force=False, verbose=False, jobs=None, tag=None, defines=()):
     jobs = jobs or os.cpu_count() or 4
     with cf.ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, defines), srcs))
-    objs = [o for o, _ in results]
+    objs = [o for o, _ in results] + [_build_id_object(obj_dir, list(defines))]
     if (force or not os.path.exists(lib)
             or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
         cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, *objs]

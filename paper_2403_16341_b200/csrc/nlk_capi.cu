@@ -75,28 +75,64 @@ int validate(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const void* 
   return NLK_OK;
 }
 
-// The refill counter is a stream-ordered 8-byte allocation.  Keep the
-// device's default pool from returning memory to the driver at every
-// synchronisation (release threshold 0 by default), or each first launch
-// after a sync pays a page mapping on the GPU timeline.
-void keep_pool_warm() {
-  static thread_local int done_dev = -1;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// Calls that take a stream run on the stream's device: the occupancy query,
+// the smem attribute, stream-ordered allocations and the launch all refer to
+// the current device, so it is switched to the stream's for the call and
+// restored after (a caller whose current device differs from the stream's
+// would otherwise launch into another device's stream).
+struct DeviceOfStream {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceOfStream(cudaStream_t s) {
+    if (s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread) return;
+    int sdev = -1, cur = -1;
+    err = cudaStreamGetDevice(s, &sdev);
+    if (err != cudaSuccess) return;
+    err = cudaGetDevice(&cur);
+    if (err != cudaSuccess || cur == sdev) return;
+    err = cudaSetDevice(sdev);
+    if (err == cudaSuccess) prev = cur;
   }
-  done_dev = dev;
+  ~DeviceOfStream() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Stream-ordered allocations (the 8-byte refill counter, the host path's
+// staging) come from a private pool per device that keeps its memory
+// (release threshold = max), so a first launch after a synchronisation pays
+// no page mapping -- without changing the policy of the device's default
+// pool, which other libraries in the process share.
+cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev & 63]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev & 63], &props);
+      if (e != cudaSuccess) return e;
+      uint64_t thr = UINT64_MAX;
+      e = cudaMemPoolSetAttribute(pools[dev & 63], cudaMemPoolAttrReleaseThreshold, &thr);
+      if (e != cudaSuccess) return e;
+    }
+    pool = pools[dev & 63];
+  }
+  return cudaMallocFromPoolAsync(ptr, bytes, pool, s);
 }
 
 int launch(nlk::Launcher l, const nlk::KernelArgs& a0, cudaStream_t s) {
   nlk::KernelArgs a = a0;
-  keep_pool_warm();
   unsigned long long* counter = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(*counter), s);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(counter)");
+  cudaError_t e = pool_alloc(reinterpret_cast<void**>(&counter), sizeof(*counter), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync(counter)");
   e = cudaMemsetAsync(counter, 0, sizeof(*counter), s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
   a.counter = counter;
@@ -131,7 +167,7 @@ Workspace& workspace(int dev) {
 
 extern "C" {
 
-int nlk_version(void) { return 100; }
+int nlk_version(void) { return 20000; }
 
 const char* nlk_last_error(void) { return g_err.c_str(); }
 
@@ -198,7 +234,55 @@ int nlk_solve_batch(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const
   a.nf = nf_out;
   a.njac = njac_out;
   a.nlinsolve = nlinsolve_out;
+  DeviceOfStream guard(static_cast<cudaStream_t>(stream));
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "stream device");
   return launch(l, a, static_cast<cudaStream_t>(stream));
+}
+
+int nlk_solve_batch_poly(int32_t handle, int32_t dtype, int64_t B, const void* u0_soa,
+                         const void* p_soa, double abstol, int32_t maxiters, void* u_out,
+                         void* resid_out, int8_t* retcode_out, int32_t* nsteps_out,
+                         int32_t* nf_out, int32_t* njac_out, int32_t* nlinsolve_out,
+                         int8_t* stage_retcodes_out, void* stream) {
+  // run_polyalgorithm (solvers.py:570-599) for n <= QN_SKIP_THRESHOLD = 25
+  // (every registered problem): the quasi-Newton stages are skipped and the
+  // stages are NR -> NR + backtracking -> trust region (solvers.py:553-565).
+  static const int32_t kStages[3] = {nlk::ALG_NR, nlk::ALG_NEWTON_LS, nlk::ALG_TR};
+  nlk::Launcher ls[3];
+  const nlk::Entry* e = nullptr;
+  for (int k = 0; k < 3; ++k) {
+    int rc = validate(handle, kStages[k], dtype, B, u0_soa, p_soa, abstol, maxiters, u_out,
+                      resid_out, retcode_out, &ls[k], &e);
+    if (rc != NLK_OK) return rc;
+  }
+  if (B > 0 && !stage_retcodes_out)
+    return fail(NLK_ERR_BAD_ARGUMENT, "stage_retcodes_out [3][B] is required");
+  if (B == 0) return NLK_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DeviceOfStream guard(st);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "stream device");
+  cudaError_t ce = cudaMemsetAsync(stage_retcodes_out, 0xff, 3 * B, st);  // -1: not run
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync(stage_retcodes)");
+  for (int k = 0; k < 3; ++k) {
+    nlk::KernelArgs a{};
+    a.B = B;
+    a.u0 = u0_soa;
+    a.p = p_soa;
+    a.abstol = abstol;
+    a.maxiters = maxiters;
+    a.u_out = u_out;
+    a.resid_out = resid_out;
+    a.retcode = retcode_out;
+    a.nsteps = nsteps_out;
+    a.nf = nf_out;
+    a.njac = njac_out;
+    a.nlinsolve = nlinsolve_out;
+    a.poly_stage = k + 1;
+    a.stage_rc = stage_retcodes_out;
+    int rc = launch(ls[k], a, st);
+    if (rc != NLK_OK) return rc;
+  }
+  return NLK_OK;
 }
 
 int nlk_solve_batch_host(int32_t handle, int32_t alg, int32_t dtype, int64_t B, const void* u0_soa,
@@ -312,14 +396,15 @@ extern "C" int nlk_solve_batch_host_async(int32_t handle, int32_t alg, int32_t d
                     retcode_out, &l, &e);
   if (rc != NLK_OK || B == 0) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  keep_pool_warm();
+  DeviceOfStream guard(st);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "stream device");
   const size_t es = dtype == NLK_F64 ? 8 : 4;
   const int n = e->n, m = e->m;
   // staging: u0 | p | u_out | resid | counters[4] | retcode
   const size_t bytes = B * es * (2 * n + m + 1) + B * 4 * 4 + B + 256;
   char* base = nullptr;
-  cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, st);
-  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMallocAsync(staging)");
+  cudaError_t ce = pool_alloc(reinterpret_cast<void**>(&base), bytes, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMallocFromPoolAsync(staging)");
   char* du0 = base;
   char* dp = du0 + B * es * n;
   char* duo = dp + B * es * m;
@@ -394,6 +479,8 @@ int nlk_ift_forward_batch(int32_t handle, int32_t dtype, int64_t B, const void* 
                       nullptr, &l);
   if (rc != NLK_OK || B == 0) return rc;
   nlk::IftArgs a{B, u_star_soa, theta_soa, nullptr, abstol, S_out, solve_resid_out, status_out};
+  DeviceOfStream guard(static_cast<cudaStream_t>(stream));
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "stream device");
   cudaError_t ce = l(a, static_cast<cudaStream_t>(stream));
   return ce == cudaSuccess ? NLK_OK : cuda_fail(ce, "ift kernel launch");
 }
@@ -407,6 +494,8 @@ int nlk_ift_adjoint_batch(int32_t handle, int32_t dtype, int64_t B, const void* 
                       gbar_soa, &l);
   if (rc != NLK_OK || B == 0) return rc;
   nlk::IftArgs a{B, u_star_soa, theta_soa, gbar_soa, abstol, grad_out, solve_resid_out, status_out};
+  DeviceOfStream guard(static_cast<cudaStream_t>(stream));
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "stream device");
   cudaError_t ce = l(a, static_cast<cudaStream_t>(stream));
   return ce == cudaSuccess ? NLK_OK : cuda_fail(ce, "ift kernel launch");
 }

@@ -15,7 +15,7 @@
 #include <stdint.h>
 #include <cstdlib>
 
-#include "nlk_coop.cuh"
+#include "nlk_solvers.cuh"
 
 namespace nlk {
 
@@ -33,6 +33,15 @@ struct KernelArgs {
   int32_t* njac;
   int32_t* nlinsolve;
   unsigned long long* counter;  // refills claimed so far (zeroed before launch)
+  // Device-side poly-algorithm (run_polyalgorithm, solvers.py:570-599): 0 for
+  // a plain solve; stage s = 1, 2, 3 for its s-th stage.  Stage 1 writes the
+  // outputs as a plain solve does; a later stage skips every system whose
+  // current best is a success, adds its counters to the running totals and
+  // replaces the best (u, resid, retcode) when it succeeds or reaches a
+  // strictly smaller residual -- min(results, key=(not success, resid_norm)).
+  // stage_rc[(s-1)*B + b] records the stage's retcode (-1: stage not run).
+  int poly_stage;
+  int8_t* stage_rc;
 };
 
 constexpr int kThreads = kSmStride;
@@ -79,78 +88,10 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const K
     if (!live) continue;
     int st;
     if (fresh) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) s.u[i] = u0[i * B + sys];
-#pragma unroll
-      for (int i = 0; i < M; ++i) s.p[i] = pp[i * B + sys];
-      st = s.init(abstol);
-      fresh = false;
-    } else {
-      st = s.step(abstol, a.maxiters);
-    }
-    if (st != RUNNING) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
-      ro[sys] = max_abs<N>(s.f);  // resid_max_norm (core.py:101-103)
-      a.retcode[sys] = static_cast<int8_t>(st);
-      if (a.nsteps) a.nsteps[sys] = s.nsteps;
-      if (a.nf) a.nf[sys] = s.nf;
-      if (a.njac) a.njac[sys] = s.njac;
-      if (a.nlinsolve) a.nlinsolve[sys] = s.nlinsolve;
-      sys = -1;
-    }
-  }
-}
-
-// Cooperative variant (nlk_coop.cuh): a group of N lanes per system, 32/N
-// systems per warp; refills are claimed per group by its row-0 lane.
-template <class P, int N, class T, int ALG>
-__global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel_coop(const KernelArgs a) {
-  using Solver = typename CoopOf<P, N, T, ALG>::type;
-  using Shape = CoopShape<N>;
-  constexpr int M = P::M;
-  constexpr int WARPS = kThreads / 32;
-  __shared__ T tbuf[WARPS][Shape::SPW][N * Shape::LD];
-  const T* __restrict__ u0 = static_cast<const T*>(a.u0);
-  const T* __restrict__ pp = static_cast<const T*>(a.p);
-  T* __restrict__ uo = static_cast<T*>(a.u_out);
-  T* __restrict__ ro = static_cast<T*>(a.resid_out);
-  const T abstol = static_cast<T>(a.abstol);
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int64_t B = a.B;
-  const bool idle = lane >= Shape::LANES;
-  const int grp = idle ? 0 : lane / N;
-
-  Solver s;
-  s.g.base = grp * N;
-  s.g.row = lane - s.g.base;
-  s.g.mask = ((1u << N) - 1u) << s.g.base;
-  s.tbuf = &tbuf[warp][grp][0];
-  const int64_t groups_total = static_cast<int64_t>(gridDim.x) * WARPS * Shape::SPW;
-  int64_t sys = idle ? B : (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * Shape::SPW + grp;
-  bool fresh = true;
-  for (;;) {
-    const bool need = !idle && sys < 0;
-    const bool leader_need = need && s.g.row == 0;
-    const unsigned want = __ballot_sync(0xffffffffu, leader_need);
-    if (want) {
-      const int leader = __ffs(want) - 1;
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned long long>(__popc(want)));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      int64_t mine = static_cast<int64_t>(groups_total + base + __popc(want & ((1u << lane) - 1u)));
-      mine = __shfl_sync(0xffffffffu, mine, idle ? lane : s.g.base);
-      if (need) {
-        sys = mine;
-        fresh = true;
+      if (a.poly_stage > 1 && a.retcode[sys] == SUCCESS) {  // an earlier stage succeeded
+        sys = -1;
+        continue;
       }
-    }
-    const bool live = !idle && sys < B;
-    if (!__any_sync(0xffffffffu, live)) break;
-    if (!live) continue;
-    int st;
-    if (fresh) {
 #pragma unroll
       for (int i = 0; i < N; ++i) s.u[i] = u0[i * B + sys];
 #pragma unroll
@@ -161,14 +102,24 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel_coop(co
       st = s.step(abstol, a.maxiters);
     }
     if (st != RUNNING) {
-      // lane r writes component r; row 0 writes the scalars
-      T ur = s.u[0];
+      const T r = max_abs<N>(s.f);  // resid_max_norm (core.py:101-103)
+      if (a.poly_stage > 1) {
+        a.stage_rc[static_cast<int64_t>(a.poly_stage - 1) * B + sys] = static_cast<int8_t>(st);
+        if (a.nsteps) a.nsteps[sys] += s.nsteps;
+        if (a.nf) a.nf[sys] += s.nf;
+        if (a.njac) a.njac[sys] += s.njac;
+        if (a.nlinsolve) a.nlinsolve[sys] += s.nlinsolve;
+        if (st == SUCCESS || r < ro[sys]) {  // NaN never compares smaller
 #pragma unroll
-      for (int i = 1; i < N; ++i)
-        if (i == s.g.row) ur = s.u[i];
-      uo[s.g.row * B + sys] = ur;
-      if (s.g.row == 0) {
-        ro[sys] = max_abs<N>(s.f);
+          for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
+          ro[sys] = r;
+          a.retcode[sys] = static_cast<int8_t>(st);
+        }
+      } else {
+        if (a.poly_stage == 1) a.stage_rc[sys] = static_cast<int8_t>(st);
+#pragma unroll
+        for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
+        ro[sys] = r;
         a.retcode[sys] = static_cast<int8_t>(st);
         if (a.nsteps) a.nsteps[sys] = s.nsteps;
         if (a.nf) a.nf[sys] = s.nf;
@@ -183,20 +134,17 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel_coop(co
 // Host-side launcher: persistent grid sized from the occupancy calculator.
 template <class P, int N, class T, int ALG>
 cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out) {
-  auto kern = [] {
-    if constexpr (UseCoop<N, ALG>::value) return solve_kernel_coop<P, N, T, ALG>;
-    else return solve_kernel<P, N, T, ALG>;
-  }();
-  constexpr int per_block_systems = UseCoop<N, ALG>::value ? (kThreads / 32) * CoopShape<N>::SPW : kThreads;
+  auto kern = solve_kernel<P, N, T, ALG>;
+  constexpr int per_block_systems = kThreads;
   // occupancy and the smem attribute are per kernel and device: computed once
-  static thread_local int cached_dev = -1, cached_sms = 0, cached_per_sm = 0;
+  // per device (per_sm_of[dev] == 0: not yet)
+  static thread_local int sms_of[64], per_sm_of[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  size_t smem = 0;
-  if constexpr (!UseCoop<N, ALG>::value)
-    smem = sizeof(T) * kThreads * SolverOf<P, N, T, ALG>::type::kSmemElems;
-  if (dev != cached_dev) {
+  dev &= 63;
+  const size_t smem = sizeof(T) * kThreads * SolverOf<P, N, T, ALG>::type::kSmemElems;
+  if (per_sm_of[dev] == 0) {
     int sms = 0, per_sm = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
@@ -215,11 +163,10 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
     }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     if (e != cudaSuccess) return e;
-    cached_dev = dev;
-    cached_sms = sms;
-    cached_per_sm = per_sm < 1 ? 1 : per_sm;
+    sms_of[dev] = sms;
+    per_sm_of[dev] = per_sm < 1 ? 1 : per_sm;
   }
-  const int sms = cached_sms, per_sm = cached_per_sm;
+  const int sms = sms_of[dev], per_sm = per_sm_of[dev];
   int64_t want = (a.B + per_block_systems - 1) / per_block_systems;
   int64_t grid = static_cast<int64_t>(per_sm) * sms;
   if (want < grid) grid = want;

@@ -49,6 +49,14 @@ class BatchSensitivity:
 
 
 def _handle(problem, n):
+    # the reference differentiates problem.analytic_jacobian when one is set
+    # (sensitivity.py:26-28); the device only has the dual-sweep Jacobian of
+    # its registered residuals, so such a problem is refused, not silently
+    # given a different Jacobian
+    if getattr(problem, "analytic_jacobian", None) is not None:
+        raise NotImplementedError("problems with an analytic_jacobian are not supported on the "
+                                  "GPU sensitivity path (the device differentiates the "
+                                  "registered residual with dual sweeps)")
     pid, nn = resolve_problem(problem, n)
     h, n_out, m = _lib.problem_lookup(pid, nn)
     if m == 0:
@@ -78,10 +86,11 @@ def ift_forward_batch(problem, u_star, theta, abstol=1e-8, full=False, n=None, d
     S = torch.empty((n * m, B), dtype=torch.float64, device=dev)
     st = torch.empty(B, dtype=torch.int8, device=dev)
     res = torch.empty(B, dtype=torch.float64, device=dev) if full else None
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    _lib.check(_lib.lib().nlk_ift_forward_batch(
-        h, 0, B, us.data_ptr(), ts.data_ptr(), float(abstol), S.data_ptr(),
-        None if res is None else res.data_ptr(), st.data_ptr(), stream))
+    with torch.cuda.device(dev):  # the legacy stream (0) means the current device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().nlk_ift_forward_batch(
+            h, 0, B, us.data_ptr(), ts.data_ptr(), float(abstol), S.data_ptr(),
+            None if res is None else res.data_ptr(), st.data_ptr(), stream))
     return BatchSensitivity(S.t().reshape(B, n, m), st, res)
 
 
@@ -97,10 +106,11 @@ def ift_adjoint_batch(problem, u_star, theta, gbar, abstol=1e-8, full=False, n=N
     G = torch.empty((m, B), dtype=torch.float64, device=dev)
     st = torch.empty(B, dtype=torch.int8, device=dev)
     res = torch.empty(B, dtype=torch.float64, device=dev) if full else None
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    _lib.check(_lib.lib().nlk_ift_adjoint_batch(
-        h, 0, B, us.data_ptr(), ts.data_ptr(), gs.data_ptr(), float(abstol), G.data_ptr(),
-        None if res is None else res.data_ptr(), st.data_ptr(), stream))
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().nlk_ift_adjoint_batch(
+            h, 0, B, us.data_ptr(), ts.data_ptr(), gs.data_ptr(), float(abstol), G.data_ptr(),
+            None if res is None else res.data_ptr(), st.data_ptr(), stream))
     return BatchSensitivity(G.t(), st, res)
 
 

@@ -142,18 +142,26 @@ class BatchResult:
     njac: torch.Tensor
     nlinsolve: torch.Tensor
     wall_time: float = 0.0
+    stage_retcodes: torch.Tensor = None  # poly-algorithm: int8 [B, 3], -1 = stage not run
 
     def to_numpy(self):
-        return {k: getattr(self, k).cpu().numpy() for k in
-                ("u", "resid", "retcode", "nsteps", "nf", "njac", "nlinsolve")}
+        out = {k: getattr(self, k).cpu().numpy() for k in
+               ("u", "resid", "retcode", "nsteps", "nf", "njac", "nlinsolve")}
+        if self.stage_retcodes is not None:
+            out["stage_retcodes"] = self.stage_retcodes.cpu().numpy()
+        return out
 
     def result(self, i):
         """SolveResult of system i (core.py:80-91)."""
         st = Stats(nf=int(self.nf[i]), njac=int(self.njac[i]), njvp=0,
                    nlinsolve=int(self.nlinsolve[i]), nsteps=int(self.nsteps[i]),
                    wall_time=self.wall_time)
+        stages = None
+        if self.stage_retcodes is not None:
+            stages = [retcode_from_int(c) for c in self.stage_retcodes[i].cpu().tolist() if c >= 0]
         return SolveResult(self.u[i].detach().cpu().numpy().astype(float),
-                           float(self.resid[i]), retcode_from_int(int(self.retcode[i])), st)
+                           float(self.resid[i]), retcode_from_int(int(self.retcode[i])), st,
+                           stage_retcodes=stages)
 
 
 _DTYPES = {torch.float64: 0, torch.float32: 1, "f64": 0, "f32": 1, np.float64: 0,
@@ -174,13 +182,43 @@ def solve_batch_soa(handle, alg, u0_soa, p_soa, abstol=1e-8, maxiters=1000, out=
                "retcode": torch.empty(B, dtype=torch.int8, device=dev),
                "counters": torch.empty((4, B), dtype=torch.int32, device=dev)}
     c = out["counters"]
-    if stream is None:
-        stream = torch.cuda.current_stream(dev).cuda_stream
-    _lib.check(_lib.lib().nlk_solve_batch(
-        handle, alg, _DTYPES[dt], B, u0_soa.data_ptr(),
-        None if p_soa is None else p_soa.data_ptr(), float(abstol), int(maxiters),
-        out["u"].data_ptr(), out["resid"].data_ptr(), out["retcode"].data_ptr(),
-        c[0].data_ptr(), c[1].data_ptr(), c[2].data_ptr(), c[3].data_ptr(), stream))
+    # the library runs on the stream's device; the legacy default stream (0)
+    # means the current device, so make it u0's
+    with torch.cuda.device(dev):
+        if stream is None:
+            stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().nlk_solve_batch(
+            handle, alg, _DTYPES[dt], B, u0_soa.data_ptr(),
+            None if p_soa is None else p_soa.data_ptr(), float(abstol), int(maxiters),
+            out["u"].data_ptr(), out["resid"].data_ptr(), out["retcode"].data_ptr(),
+            c[0].data_ptr(), c[1].data_ptr(), c[2].data_ptr(), c[3].data_ptr(), stream))
+    return out
+
+
+def solve_batch_poly_soa(handle, u0_soa, p_soa, abstol=1e-8, maxiters=1000, out=None,
+                         stream=None):
+    """The batched default poly-algorithm (nlk_solve_batch_poly): SoA device
+    tensors in; the dict of solve_batch_soa plus ``stage_retcodes`` int8
+    [3, B] (-1 = stage not run)."""
+    n, B = u0_soa.shape
+    dt = u0_soa.dtype
+    dev = u0_soa.device
+    if out is None:
+        out = {"u": torch.empty((n, B), dtype=dt, device=dev),
+               "resid": torch.empty(B, dtype=dt, device=dev),
+               "retcode": torch.empty(B, dtype=torch.int8, device=dev),
+               "counters": torch.empty((4, B), dtype=torch.int32, device=dev),
+               "stage_retcodes": torch.empty((3, B), dtype=torch.int8, device=dev)}
+    c = out["counters"]
+    with torch.cuda.device(dev):
+        if stream is None:
+            stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().nlk_solve_batch_poly(
+            handle, _DTYPES[dt], B, u0_soa.data_ptr(),
+            None if p_soa is None else p_soa.data_ptr(), float(abstol), int(maxiters),
+            out["u"].data_ptr(), out["resid"].data_ptr(), out["retcode"].data_ptr(),
+            c[0].data_ptr(), c[1].data_ptr(), c[2].data_ptr(), c[3].data_ptr(),
+            out["stage_retcodes"].data_ptr(), stream))
     return out
 
 
@@ -233,7 +271,7 @@ def solve_batch(problem, u0, p=None, algorithm="newton-raphson", options=None,
     u0_soa = u0.t().contiguous()
     t0 = time.perf_counter()
     if algorithm == "polyalgorithm" or algorithm is None:
-        out = _polyalgorithm(handle, u0_soa, p_soa, options)
+        out = solve_batch_poly_soa(handle, u0_soa, p_soa, options.abstol, options.maxiters)
     else:
         spec = resolve_algorithm(algorithm)
         out = solve_batch_soa(handle, spec.kernel, u0_soa, p_soa, options.abstol,
@@ -241,41 +279,9 @@ def solve_batch(problem, u0, p=None, algorithm="newton-raphson", options=None,
     torch.cuda.current_stream(device).synchronize()
     wall = time.perf_counter() - t0
     c = out["counters"]
+    sr = out.get("stage_retcodes")
     return BatchResult(out["u"].t(), out["resid"], out["retcode"], c[0], c[1], c[2], c[3],
-                       wall)
-
-
-def _polyalgorithm(handle, u0_soa, p_soa, options):
-    """Batched run_polyalgorithm (solvers.py:570-599) for n <= 25: stages
-    NR -> NR+backtracking -> TR, each on the systems every earlier stage left
-    unsolved (compacted), with the reference's result selection
-    min(results, key=(not success, resid_norm)) and summed counters."""
-    n, B = u0_soa.shape
-    best = solve_batch_soa(handle, 0, u0_soa, p_soa, options.abstol, options.maxiters)
-    best = {k: v.clone() for k, v in best.items()}
-    best_succ = best["retcode"] == 0
-    totals = best["counters"].clone()
-    for stage in POLY_STAGES[1:]:
-        idx = torch.nonzero(~best_succ, as_tuple=False).flatten()
-        if idx.numel() == 0:
-            break
-        sub_u0 = u0_soa[:, idx].contiguous()
-        sub_p = None if p_soa is None else p_soa[:, idx].contiguous()
-        r = solve_batch_soa(handle, ALGORITHM_PRESETS[stage].kernel, sub_u0, sub_p,
-                            options.abstol, options.maxiters)
-        totals[:, idx] += r["counters"]
-        succ = r["retcode"] == 0
-        old_res = best["resid"][idx]
-        # Python tuple ordering of (not success, resid): replace only when
-        # strictly smaller (NaN never compares smaller, so it is kept if first)
-        better = succ | (r["resid"] < old_res)
-        take = idx[better]
-        best["u"][:, take] = r["u"][:, better]
-        best["resid"][take] = r["resid"][better]
-        best["retcode"][take] = r["retcode"][better]
-        best_succ[idx] = best_succ[idx] | succ
-    best["counters"] = totals
-    return best
+                       wall, None if sr is None else sr.t())
 
 
 def run_algorithm(problem, spec, options=None):
