@@ -43,16 +43,17 @@ def test_poly_result_to_json(name):
 
 
 @pytest.mark.parametrize("index,sigma,B", [(11, 0.1, 20000), (16, 1.0, 5000), (22, 1.0, 20000),
-                                           (15, 1.0, 5000), (5, 1.0, 5000)])
+                                           (15, 1.0, 5000), (5, 1.0, 5000), (4, 1.0, 5000)])
 def test_poly_oracle_c2(index, sigma, B):
     from oracle import oracle as O
     b = W.c2_suite(index, 0, B, sigma)
     ref = O.poly_batch(b.problem_id, b.u0)
     got = gpu_poly(b.problem_id, b.u0).to_numpy()
-    check_poly_fields(ref, got, f"#{index} sigma={sigma}")
+    check_poly_fields(ref, got, f"#{index} sigma={sigma}",
+                      later_stages=index in (11, 15, 16, 22))
 
 
-def check_poly_fields(ref, got, what):
+def check_poly_fields(ref, got, what, later_stages=True):
     bits = lambda a: np.ascontiguousarray(a, np.float64).view(np.int64)  # noqa: E731
     same = np.ones(len(ref["retcode"]), bool)
     for k in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
@@ -62,8 +63,8 @@ def check_poly_fields(ref, got, what):
     same &= bits(got["resid"]) == bits(ref["resid"])
     bad = np.nonzero(~same)[0]
     assert len(bad) == 0, f"{what}: {len(bad)} systems differ (e.g. {bad[:8]})"
-    # the fixtures must reach the later stages
-    assert (ref["stage_retcodes"][:, 1] >= 0).any()
+    if later_stages:  # the inputs must reach the later stages
+        assert (ref["stage_retcodes"][:, 1] >= 0).any()
 
 
 def test_poly_rosenbrock_wide_oracle():
