@@ -49,6 +49,37 @@ constexpr int kThreads = kSmStride;
 #define NLK_MIN_BLOCKS 1
 #endif
 
+// Result of a finished system: written as a plain solve, or merged into the
+// running poly-algorithm state (KernelArgs::poly_stage).
+template <int N, class T, class S>
+__device__ __forceinline__ void finish(const KernelArgs& a, const S& s, int st, int64_t sys,
+                                       int64_t B, T* __restrict__ uo, T* __restrict__ ro) {
+  const T r = max_abs<N>(s.f);  // resid_max_norm (core.py:101-103)
+  if (a.poly_stage > 1) {
+    a.stage_rc[static_cast<int64_t>(a.poly_stage - 1) * B + sys] = static_cast<int8_t>(st);
+    if (a.nsteps) a.nsteps[sys] += s.nsteps;
+    if (a.nf) a.nf[sys] += s.nf;
+    if (a.njac) a.njac[sys] += s.njac;
+    if (a.nlinsolve) a.nlinsolve[sys] += s.nlinsolve;
+    if (st == SUCCESS || r < ro[sys]) {  // NaN never compares smaller
+#pragma unroll
+      for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
+      ro[sys] = r;
+      a.retcode[sys] = static_cast<int8_t>(st);
+    }
+  } else {
+    if (a.poly_stage == 1) a.stage_rc[sys] = static_cast<int8_t>(st);
+#pragma unroll
+    for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
+    ro[sys] = r;
+    a.retcode[sys] = static_cast<int8_t>(st);
+    if (a.nsteps) a.nsteps[sys] = s.nsteps;
+    if (a.nf) a.nf[sys] = s.nf;
+    if (a.njac) a.njac[sys] = s.njac;
+    if (a.nlinsolve) a.nlinsolve[sys] = s.nlinsolve;
+  }
+}
+
 template <class P, int N, class T, int ALG>
 __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const KernelArgs a) {
   using Solver = typename SolverOf<P, N, T, ALG>::type;
@@ -102,39 +133,88 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const K
       st = s.step(abstol, a.maxiters);
     }
     if (st != RUNNING) {
-      const T r = max_abs<N>(s.f);  // resid_max_norm (core.py:101-103)
-      if (a.poly_stage > 1) {
-        a.stage_rc[static_cast<int64_t>(a.poly_stage - 1) * B + sys] = static_cast<int8_t>(st);
-        if (a.nsteps) a.nsteps[sys] += s.nsteps;
-        if (a.nf) a.nf[sys] += s.nf;
-        if (a.njac) a.njac[sys] += s.njac;
-        if (a.nlinsolve) a.nlinsolve[sys] += s.nlinsolve;
-        if (st == SUCCESS || r < ro[sys]) {  // NaN never compares smaller
-#pragma unroll
-          for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
-          ro[sys] = r;
-          a.retcode[sys] = static_cast<int8_t>(st);
-        }
-      } else {
-        if (a.poly_stage == 1) a.stage_rc[sys] = static_cast<int8_t>(st);
-#pragma unroll
-        for (int i = 0; i < N; ++i) uo[i * B + sys] = s.u[i];
-        ro[sys] = r;
-        a.retcode[sys] = static_cast<int8_t>(st);
-        if (a.nsteps) a.nsteps[sys] = s.nsteps;
-        if (a.nf) a.nf[sys] = s.nf;
-        if (a.njac) a.njac[sys] = s.njac;
-        if (a.nlinsolve) a.nlinsolve[sys] = s.nlinsolve;
-      }
+      finish<N>(a, s, st, sys, B, uo, ro);
       sys = -1;
     }
   }
 }
 
+// Static schedule for problem families whose iteration counts are tight
+// (P::kStaticSchedule, e.g. the parametrised quadratic of C1/C5: 4-8 Newton
+// steps on every system).  Each thread takes systems by grid stride and runs
+// each to completion: a warp's lanes always hold consecutive systems, so
+// every load and store of the SoA batch is one coalesced transaction, and
+// there is no per-iteration refill bookkeeping (ballot, vote, atomics).  The
+// price is that a warp runs as long as its slowest lane -- the reason the
+// heavy-tailed suite problems keep the refilling kernel above.
+#ifndef NLK_STATIC_PREFETCH_MAX
+#define NLK_STATIC_PREFETCH_MAX 16
+#endif
+template <class P, int N, class T, int ALG>
+__global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel_static(const KernelArgs a) {
+  using Solver = typename SolverOf<P, N, T, ALG>::type;
+  constexpr int M = P::M;
+  const T* __restrict__ u0 = static_cast<const T*>(a.u0);
+  const T* __restrict__ pp = static_cast<const T*>(a.p);
+  T* __restrict__ uo = static_cast<T*>(a.u_out);
+  T* __restrict__ ro = static_cast<T*>(a.resid_out);
+  const T abstol = static_cast<T>(a.abstol);
+  const int64_t B = a.B;
+  Solver s;
+  if constexpr (Solver::kSmemElems > 0) {
+    extern __shared__ __align__(16) unsigned char nlk_dyn_smem[];
+    s.sm = reinterpret_cast<T*>(nlk_dyn_smem) + threadIdx.x;
+  }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t sys = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // the next system's inputs are loaded before the current one is solved, so
+  // their DRAM latency hides behind the solve (small N + M: registers)
+  constexpr bool PF = N + M <= NLK_STATIC_PREFETCH_MAX;
+  T nu[PF ? N : 1], np_[PF && M > 0 ? M : 1];
+  auto load = [&](int64_t i, T* uu, T* pv) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) uu[k] = u0[k * B + i];
+#pragma unroll
+    for (int k = 0; k < M; ++k) pv[k] = pp[k * B + i];
+  };
+  if constexpr (PF) {
+    if (sys < B) load(sys, nu, np_);
+  }
+  for (; sys < B; sys += stride) {
+    if constexpr (PF) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) s.u[k] = nu[k];
+#pragma unroll
+      for (int k = 0; k < M; ++k) s.p[k] = np_[k];
+      if (sys + stride < B) load(sys + stride, nu, np_);
+    } else {
+      load(sys, s.u, s.p);
+    }
+    if (a.poly_stage > 1 && a.retcode[sys] == SUCCESS) continue;  // an earlier stage succeeded
+    int st = s.init(abstol);
+    while (st == RUNNING) st = s.step(abstol, a.maxiters);
+    finish<N>(a, s, st, sys, B, uo, ro);
+  }
+}
+
+// NLK_SCHEDULE_STATIC_ALL=1 (variant builds): every kernel static
+#ifndef NLK_SCHEDULE_STATIC_ALL
+#define NLK_SCHEDULE_STATIC_ALL 0
+#endif
+#ifndef NLK_SCHEDULE_STATIC
+#define NLK_SCHEDULE_STATIC 1
+#endif
+template <class P> struct UseStatic {
+  static constexpr bool value = NLK_SCHEDULE_STATIC_ALL || (NLK_SCHEDULE_STATIC && StaticSchedule<P>::value);
+};
+
 // Host-side launcher: persistent grid sized from the occupancy calculator.
 template <class P, int N, class T, int ALG>
 cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out) {
-  auto kern = solve_kernel<P, N, T, ALG>;
+  auto kern = [] {
+    if constexpr (UseStatic<P>::value) return solve_kernel_static<P, N, T, ALG>;
+    else return solve_kernel<P, N, T, ALG>;
+  }();
   constexpr int per_block_systems = kThreads;
   // occupancy and the smem attribute are per kernel and device: computed once
   // per device (per_sm_of[dev] == 0: not yet)

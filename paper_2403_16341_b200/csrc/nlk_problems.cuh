@@ -193,6 +193,13 @@ template <class P>
 struct JacRankOneDiag<P, std::void_t<decltype(P::kJacRankOneDiag)>> {
   static constexpr bool value = P::kJacRankOneDiag;
 };
+// Problems whose iteration counts are tight run on the static (grid-stride)
+// schedule of nlk_kernel.cuh instead of the refilling one
+template <class P, class = void> struct StaticSchedule { static constexpr bool value = false; };
+template <class P>
+struct StaticSchedule<P, std::void_t<decltype(P::kStaticSchedule)>> {
+  static constexpr bool value = P::kStaticSchedule;
+};
 template <class P, class = void> struct MemoOf { static constexpr int value = 0; };
 template <class P> struct MemoOf<P, std::void_t<decltype(P::kMemo)>> { static constexpr int value = P::kMemo; };
 
@@ -624,6 +631,8 @@ struct GeneralizedRosenbrock {  // 363-368
 template <int NN>
 struct Quadratic {  // 382-383: u * u - theta
   static constexpr int N = NN, M = NN;
+  // C1/C5 iteration counts are tight (4-8 steps): grid-stride schedule
+  static constexpr bool kStaticSchedule = true;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T* p, S* out, C& cx) {
 #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];

@@ -236,7 +236,8 @@ struct Base {
 template <class P, int N, class T, bool LS>
 struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
   using B = Base<P, N, T, true, NLK_SINCOS_PAIRS_NR>;
-  static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_NR_MIN>::value;
+  static constexpr bool SM =
+      UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_NR_MIN>::value;
   static constexpr int kSmemElems = SM ? N * N + N : 0;
   NLK_FD int init(T abstol) { return B::start(abstol); }
   NLK_FD int step(T abstol, int maxiters) {
@@ -322,7 +323,8 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR>;
-  static constexpr bool SM = UseSmemLU<N, T, NLK_SMEM_TR_MIN>::value;
+  static constexpr bool SM =
+      UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_TR_MIN>::value;
   // JSM: J also in shared memory (after LU and rhs) instead of registers
   static constexpr bool JSM =
       SM && NLK_TR_JSMEM && sizeof(T) * (2 * N * N + N) * kSmStride <= 227 * 1024;

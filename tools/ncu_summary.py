@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 KEYS = [
-    ("gpu__time_duration.sum", "duration (ns)"),
+    ("gpu__time_duration.sum", "duration"),
     ("launch__registers_per_thread", "registers/thread"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe inst % of peak"),
@@ -32,15 +32,18 @@ def main(path):
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))  # ncu scales units per report (ns/us/ms, byte/Kbyte/...)
     for vals in rows[2:]:
-        summarize(path, dict(zip(hdr, vals)))
+        summarize(path, dict(zip(hdr, vals)), units)
 
 
-def summarize(path, d):
+def summarize(path, d, units):
     print(f"== {path}  kernel: {d.get('Kernel Name', '?')[:90]}")
     for k, label in KEYS:
         if k in d:
-            print(f"  {label:32s} {d[k]}")
+            u = units.get(k, "")
+            lab = f"{label} ({u})" if u and u not in ("%",) else label
+            print(f"  {lab:32s} {d[k]}")
     stalls = []
     for k, v in d.items():
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
