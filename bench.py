@@ -78,6 +78,11 @@ def iter_job_groups(config, lo, hi):
             yield [(b.problem_id, n, alg, b) for alg in ("broyden", "klement")]
     elif config == "c4":
         yield [("test23/broyden-tridiagonal", 16, "dfsane", W.c4_tridiagonal(lo, hi))]
+    elif config == "n16":
+        b = W.c3_rosenbrock(16, lo, hi)
+        yield [(b.problem_id, 16, alg, b) for alg in ("newton-raphson", "trust-region")]
+        b = W.c4_tridiagonal(lo, hi)
+        yield [(b.problem_id, 16, alg, b) for alg in ("newton-raphson", "trust-region")]
     elif config == "c5":
         b = W.c5_quadratic(lo, hi)
         algs = W.c5_algorithms(lo, hi)
@@ -101,6 +106,8 @@ WORKLOAD = {
     "c3": "C3: generalized Rosenbrock n=8/16 x B, u0~U[0,1)^n, {SimpleBroyden, SimpleKlement}",
     "c4": "C4: broyden-tridiagonal n=16 x B, u0=-1+0.1U(-1,1)^16, SimpleDFSane",
     "c5": "C5: u^2 - p (n=4) x B, algorithm = i mod 5 over all Simple* solvers",
+    "n16": "n=16 Newton/trust region: generalized Rosenbrock (C3 inputs) and broyden-tridiagonal "
+           "(C4 inputs) x B, {SimpleNewtonRaphson, SimpleTrustRegion}",
 }
 
 
@@ -635,7 +642,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "n16"])
     ap.add_argument("--batch", type=int, default=1 << 20, help="systems per job per GPU")
     ap.add_argument("--abstol", type=float, default=None,
                     help="default 1e-8 (f32 on the quadratics: 1e-6)")

@@ -44,7 +44,10 @@ struct KernelArgs {
   int8_t* stage_rc;
 };
 
-constexpr int kThreads = kSmStride;
+// threads per block: the solver's shared-memory slice stride (128, or 64/32
+// for the n >= 14 fp64 shared-memory LU)
+template <class P, int N, class T, int ALG>
+constexpr int block_of() { return SolverOf<P, N, T, ALG>::type::kStride; }
 #ifndef NLK_MIN_BLOCKS
 #define NLK_MIN_BLOCKS 1
 #endif
@@ -81,7 +84,7 @@ __device__ __forceinline__ void finish(const KernelArgs& a, const S& s, int st, 
 }
 
 template <class P, int N, class T, int ALG>
-__global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const KernelArgs a) {
+__global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solve_kernel(const KernelArgs a) {
   using Solver = typename SolverOf<P, N, T, ALG>::type;
   constexpr int M = P::M;
   const T* __restrict__ u0 = static_cast<const T*>(a.u0);
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel(const K
 #define NLK_STATIC_PREFETCH_MAX 16
 #endif
 template <class P, int N, class T, int ALG>
-__global__ void __launch_bounds__(kThreads, NLK_MIN_BLOCKS) solve_kernel_static(const KernelArgs a) {
+__global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solve_kernel_static(const KernelArgs a) {
   using Solver = typename SolverOf<P, N, T, ALG>::type;
   constexpr int M = P::M;
   const T* __restrict__ u0 = static_cast<const T*>(a.u0);
@@ -215,6 +218,7 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
     if constexpr (UseStatic<P>::value) return solve_kernel_static<P, N, T, ALG>;
     else return solve_kernel<P, N, T, ALG>;
   }();
+  constexpr int kThreads = block_of<P, N, T, ALG>();
   constexpr int per_block_systems = kThreads;
   // occupancy and the smem attribute are per kernel and device: computed once
   // per device (per_sm_of[dev] == 0: not yet)

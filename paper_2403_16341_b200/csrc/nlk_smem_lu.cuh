@@ -59,17 +59,18 @@ namespace nlk {
 constexpr int kSmStride = 128;
 
 // column-major N x N matrix in a strided per-thread shared-memory slice
-template <int N, class T>
+// (S = the block size: element e of thread t at smem[e * S + t])
+template <int N, class T, int S = kSmStride>
 struct SMat {
   T* base;
-  NLK_FD T& operator()(int i, int j) const { return base[(i + j * N) * kSmStride]; }
-  NLK_FD T& v(int i) const { return base[i * kSmStride]; }  // as a vector
+  NLK_FD T& operator()(int i, int j) const { return base[(i + j * N) * S]; }
+  NLK_FD T& v(int i) const { return base[i * S]; }  // as a vector
 };
 
-template <int N, class T> NLK_FD T mat_at(const SMat<N, T>& A, int e) { return A.v(e); }
+template <int N, class T, int S> NLK_FD T mat_at(const SMat<N, T, S>& A, int e) { return A.v(e); }
 
-template <int N, class T>
-NLK_FD void sm_swap_rows(const SMat<N, T>& A, int r1, int r2, int c0, int c1) {
+template <int N, class T, int S>
+NLK_FD void sm_swap_rows(const SMat<N, T, S>& A, int r1, int r2, int c0, int c1) {
 NLK_SMU
   for (int k = c0; k < c1; ++k) {
     T t = A(r1, k);
@@ -114,8 +115,8 @@ template <int N> NLK_FD uint64_t perm_compose(uint64_t A, uint64_t B) {
   return r;
 }
 // rows r0..N-1 of column c <- rows perm_get(R, r) (rows below r0 are fixed)
-template <int N, class T>
-NLK_FD void sm_gather_col(const SMat<N, T>& A, uint64_t R, int r0, int c) {
+template <int N, class T, int S>
+NLK_FD void sm_gather_col(const SMat<N, T, S>& A, uint64_t R, int r0, int c) {
   T col[N];
 NLK_SMU
   for (int r = r0; r < N; ++r) col[r] = A(perm_get(R, r), c);
@@ -125,8 +126,8 @@ NLK_SMU
 
 // GETF2 on rows OFF..N-1, columns OFF..OFF+NC-1; piv holds absolute rows.
 // Returns the panel's interchanges composed (perm_* form).
-template <int N, class T>
-NLK_FD uint64_t sm_getf2(const SMat<N, T>& A, int OFF, int NC, int* piv) {
+template <int N, class T, int S>
+NLK_FD uint64_t sm_getf2(const SMat<N, T, S>& A, int OFF, int NC, int* piv) {
   const int M = N - OFF;
   uint64_t R = perm_identity<N>();
 NLK_SMU
@@ -254,8 +255,8 @@ NLK_SMU
 }
 
 // C(rows r0.., cols c0..) -= A(rows r0.., cols k0..k0+KK) * B(rows k0.., cols c0..)
-template <int N, class T>
-NLK_FD void sm_gemm_minus(const SMat<N, T>& A, int r0, int MI, int c0, int NJ, int k0, int KK) {
+template <int N, class T, int S>
+NLK_FD void sm_gemm_minus(const SMat<N, T, S>& A, int r0, int MI, int c0, int NJ, int k0, int KK) {
 NLK_SMU
   for (int i = 0; i < MI; ++i)
 NLK_SMU
@@ -269,8 +270,8 @@ NLK_SMU
 
 // TRSM_LT (unit L) on rows IS..IS+BK-1, columns C0..N-1; sub-blocks follow
 // the bits of BK (BK <= 8 here, so no 16-blocks)
-template <int N, class T>
-NLK_FD void sm_trsm(const SMat<N, T>& A, int IS, int BK) {
+template <int N, class T, int S>
+NLK_FD void sm_trsm(const SMat<N, T, S>& A, int IS, int BK) {
   const int C0 = IS + BK, NJ = N - C0;
   int kk = 0;
 NLK_SMU
@@ -290,8 +291,8 @@ NLK_SMU
   }
 }
 
-template <int N, class T>
-NLK_FD void sm_getrf(const SMat<N, T>& A, int* piv) {
+template <int N, class T, int S>
+NLK_FD void sm_getrf(const SMat<N, T, S>& A, int* piv) {
   constexpr int BLK = ((N / 2 + 1) / 2) * 2;
   if constexpr (BLK <= 4) {
     sm_getf2(A, 0, N, piv);
@@ -341,8 +342,8 @@ NLK_SMU
 // checks, so max|A| is finite and the scan below can only reject an all-zero
 // matrix -- which getrf rejects anyway (every pivot is zero), with the same
 // outcome (SingularMatrix -> LINSOLVE_FAILED).  The scan is skipped then.
-template <int N, bool JAC_CHECKED, class T>
-NLK_FD bool sm_lu_factor(const SMat<N, T>& A, int* piv) {
+template <int N, bool JAC_CHECKED, class T, int S>
+NLK_FD bool sm_lu_factor(const SMat<N, T, S>& A, int* piv) {
   if constexpr (!JAC_CHECKED) {
     T anorm = T(0);
     bool nan = false;
@@ -366,8 +367,8 @@ NLK_SMU
 }
 
 // getrs with the right-hand side in the strided vector b (N elements)
-template <int N, class T>
-NLK_FD void sm_getrs(const SMat<N, T>& LU, const int* piv, const SMat<N, T>& b) {
+template <int N, class T, int S>
+NLK_FD void sm_getrs(const SMat<N, T, S>& LU, const int* piv, const SMat<N, T, S>& b) {
 #if NLK_LU_GATHER
   {
     uint64_t R = perm_identity<N>();
@@ -434,13 +435,18 @@ NLK_SMU
 #endif
 }
 
-// smem path when n >= NLK_SMEM_LU_MIN and the N*N + N slice of a 128-thread
-// block fits in 200 KB (f64: n <= 14; larger n keep the register path)
+// smem path when n >= MIN_N and the N*N + N slice of one block fits in
+// 200 KB.  The block size (= slice stride) is 128 threads where it fits
+// (f64: n <= 13; f32: n <= 18), else 64 or 32: n = 14..16 in f64 run 32-thread
+// blocks (69.6 KB each at n = 16, three per SM) rather than a register LU
+// whose 256 doubles spill (17.6 KB of spill stores per thread at n = 16).
 template <int N, class T, int MIN_N> struct UseSmemLU {
-  static constexpr bool value =
-      N >= MIN_N && sizeof(T) * (N * N + N) * kSmStride <= 200 * 1024;
-  // GETF2 panels need blocking <= 8 (getrf_single recursion depth 1)
-  static_assert(!value || N <= 17, "shared-memory getrf models one blocking level");
+  static constexpr int kSlice = sizeof(T) * (N * N + N);
+  static constexpr int stride = kSlice * 128 <= 200 * 1024 ? 128
+                              : kSlice * 64 <= 200 * 1024 ? 64
+                              : kSlice * 32 <= 200 * 1024 ? 32 : 0;
+  // the pivot permutation packs 4-bit row indices into a uint64 (perm_*)
+  static constexpr bool value = N >= MIN_N && stride > 0 && N <= 16;
 };
 
 #undef NLK_SMU

@@ -73,7 +73,7 @@ template <int N> struct SweepWidth {
 
 // J sinks: register array or shared-memory slice (column-major, e = i + j*N)
 template <class T> NLK_FD void jput(T* J, int e, T v) { J[e] = v; }
-template <int N, class T> NLK_FD void jput(const SMat<N, T>& J, int e, T v) { J.v(e) = v; }
+template <int N, class T, int S> NLK_FD void jput(const SMat<N, T, S>& J, int e, T v) { J.v(e) = v; }
 
 // A Jacobian whose off-diagonal entries of each column share one value
 // (problems with kJacRankOneDiag): diagonal d, column values s, and the
@@ -201,7 +201,8 @@ struct Base {
   T p[M > 0 ? M : 1];
   int k, nsteps, nf, njac, nlinsolve;
   static constexpr int kSmemElems = 0;
-  T* sm;  // this thread's shared-memory slice (stride kSmStride), see kSmemElems
+  static constexpr int kStride = kSmStride;  // block size = stride of the smem slices
+  T* sm;  // this thread's shared-memory slice (stride kStride), see kSmemElems
 
   static constexpr int KM = MEMO ? MemoOf<P>::value : 0;
   T memo[KM > 0 ? KM : 1];  // transcendentals of the last F call
@@ -236,9 +237,11 @@ struct Base {
 template <class P, int N, class T, bool LS>
 struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
   using B = Base<P, N, T, true, NLK_SINCOS_PAIRS_NR>;
-  static constexpr bool SM =
-      UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_NR_MIN>::value;
+  using SL = UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_NR_MIN>;
+  static constexpr bool SM = SL::value;
   static constexpr int kSmemElems = SM ? N * N + N : 0;
+  static constexpr int kStride = SM ? SL::stride : kSmStride;
+  using Mat = SMat<N, T, kStride>;
   NLK_FD int init(T abstol) { return B::start(abstol); }
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
@@ -246,7 +249,7 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
     T Jf[LS ? N * N : 1];  // J kept for the line search's J @ du
     T du[N];
     if constexpr (SM) {  // J streams column by column into the smem slice
-      const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
+      const Mat A{B::sm}, rhs{B::sm + N * N * kStride};
       if (B::jac(A) >= 0) return NONFINITE;
       if constexpr (LS) {
 #pragma unroll
@@ -323,11 +326,13 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR>;
-  static constexpr bool SM =
-      UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_TR_MIN>::value;
+  using SL = UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_TR_MIN>;
+  static constexpr bool SM = SL::value;
+  static constexpr int kStride = SM ? SL::stride : kSmStride;
+  using Mat = SMat<N, T, kStride>;
   // JSM: J also in shared memory (after LU and rhs) instead of registers
   static constexpr bool JSM =
-      SM && NLK_TR_JSMEM && sizeof(T) * (2 * N * N + N) * kSmStride <= 227 * 1024;
+      SM && NLK_TR_JSMEM && sizeof(T) * (2 * N * N + N) * kStride <= 227 * 1024;
   static constexpr int kSmemElems = SM ? (JSM ? 2 * N * N + N : N * N + N) : 0;
   // RD: a rank-one-plus-diagonal Jacobian kept as RDJac (2N values instead of
   // N^2 registers; test23/trigonometric: the cached J was what spilled)
@@ -338,7 +343,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   T J[(JSM || RD) ? 1 : N * N], LU[SM ? 1 : N * N];
   RDJac<N, T> jrd[RD ? 1 : 0];
   NLK_FD auto jmat() {
-    if constexpr (JSM) return SMat<N, T>{B::sm + (N * N + N) * kSmStride};
+    if constexpr (JSM) return Mat{B::sm + (N * N + N) * kStride};
     else if constexpr (RD) return RDRef<N, T, true>{&jrd[0]};
     else return static_cast<T*>(J);
   }
@@ -368,7 +373,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   NLK_FD void dogleg_plain(T* out) {
     T newton[N];
     if constexpr (SM) {
-      const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
+      const Mat A{B::sm}, rhs{B::sm + N * N * kStride};
 #pragma unroll
       for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
       sm_getrs<N>(A, piv, rhs);
@@ -430,7 +435,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   T nnorm, gg, t_star, cnorm;
   int dl;
   NLK_FD void dogleg_cached(T* out) {
-    const SMat<N, T> A{B::sm}, rhs{B::sm + N * N * kSmStride};
+    const Mat A{B::sm}, rhs{B::sm + N * N * kStride};
     if (dl == 0) {
 #pragma unroll
       for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
@@ -498,7 +503,7 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
       if constexpr (RD) jrd[0].reset();
       if (B::jac(jmat()) >= 0) return NONFINITE;
       if constexpr (SM) {
-        const SMat<N, T> A{B::sm};
+        const Mat A{B::sm};
         with_j([&](auto Jm) {
 #pragma unroll
           for (int e = 0; e < N * N; ++e) A.v(e) = mat_at(Jm, e);
