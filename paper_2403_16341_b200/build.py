@@ -102,16 +102,23 @@ def _build_id_object(obj_dir, defines):
     return obj
 
 
-def build(force=False, verbose=False, jobs=None, tag=None, defines=()):
+def build(force=False, verbose=False, jobs=None, tag=None, defines=(), only=None):
     """Compile and link; ``tag``/``defines`` make a variant library
-    ``libnlk_b200_<tag>.so`` (objects in ``_obj_<tag>``) for A/B timing."""
+    ``libnlk_b200_<tag>.so`` (objects in ``_obj_<tag>``) for A/B timing.
+    ``only`` (variants): recompile just the sources whose name contains one
+    of these substrings and link the default build's objects for the rest."""
     obj_dir, lib = (OBJ, LIB) if not tag else (OBJ + "_" + tag, LIB.replace(".so", f"_{tag}.so"))
     os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = jobs or os.cpu_count() or 4
+    mine = [s for s in srcs if not only or any(k in os.path.basename(s) for k in only)]
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, defines), srcs))
-    objs = [o for o, _ in results] + [_build_id_object(obj_dir, list(defines))]
+        results = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, defines), mine))
+    objs = [o for o, _ in results]
+    if only:  # the rest from the default build (must be current)
+        objs += [os.path.join(OBJ, os.path.basename(s).replace(".cu", ".o")) for s in srcs
+                 if s not in mine]
+    objs += [_build_id_object(obj_dir, list(defines))]
     if (force or not os.path.exists(lib)
             or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
         cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, *objs]
@@ -128,8 +135,10 @@ def main(argv=None):
     ap.add_argument("-j", "--jobs", type=int, default=None)
     ap.add_argument("--tag", default=None, help="variant name (separate objects and .so)")
     ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for nvcc")
+    ap.add_argument("--only", action="append", default=None,
+                    help="variant: recompile only sources containing this substring")
     a = ap.parse_args(argv)
-    print(build(a.force, a.verbose, a.jobs, a.tag, a.defines))
+    print(build(a.force, a.verbose, a.jobs, a.tag, a.defines, a.only))
 
 
 if __name__ == "__main__":

@@ -30,6 +30,8 @@ struct Registry {
   std::vector<const nlk::Entry*> all;
   Registry() {
     const nlk::EntryTable tables[] = {nlk::registry_suite_a(), nlk::registry_suite_b(),
+                                      nlk::registry_suite_b2(), nlk::registry_suite_b3(),
+                                      nlk::registry_suite_b4(),
                                       nlk::registry_suite_c(), nlk::registry_families_a(),
                                       nlk::registry_families_b(), nlk::registry_families_c(),
                                       nlk::registry_families_d(), nlk::registry_families_e()};

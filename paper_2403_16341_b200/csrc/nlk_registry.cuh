@@ -39,6 +39,9 @@ struct EntryTable {
 
 EntryTable registry_suite_a();
 EntryTable registry_suite_b();
+EntryTable registry_suite_b2();
+EntryTable registry_suite_b3();
+EntryTable registry_suite_b4();
 EntryTable registry_suite_c();
 EntryTable registry_families_a();
 EntryTable registry_families_b();
