@@ -1,3 +1,4 @@
+// SPDX-License-Identifier: BSD-3-Clause (SVML-derived; see NOTICE)
 // ORACLE / TEST INFRASTRUCTURE ONLY.
 //
 // numpy's float64 arctan as the reference host evaluates it: numpy 2.3 on an

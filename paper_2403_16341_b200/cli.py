@@ -149,7 +149,26 @@ def _write_csv(path, header, rows):
             fh.close()
 
 
+# Reference presets and problems that exist in nlkit (solvers.py:610-637,
+# 640-655; problems.py:390-474) but deliberately have no batched kernel: they
+# are not "unknown" (exit 2) but "not ported" (exit 3, EXIT_NOT_PORTED).
+EXIT_NOT_PORTED = 3
+REFERENCE_ONLY_PRESETS = ("newton-fd", "newton-sparse", "newton-sparse-fd", "newton-krylov",
+                          "newton-krylov-ilu0", "trust-region-nw", "levenberg-marquardt",
+                          "lm-cholesky", "lm-geodesic", "halley", "potra-ptak",
+                          "broyden-true-jac", "lbroyden", "pseudo-transient")
+REFERENCE_ONLY_PROBLEMS = ("brusselator2d",)
+
+
 def cmd_solve(args):
+    if args.problem.split("?", 1)[0] in REFERENCE_ONLY_PROBLEMS:
+        print(f"error: reference problem {args.problem!r} has no device residual "
+              "(n = 2N^2 is outside the batched small-system path; not ported)", file=sys.stderr)
+        return EXIT_NOT_PORTED
+    if args.algorithm in REFERENCE_ONLY_PRESETS:
+        print(f"error: reference preset {args.algorithm!r} has no batched GPU kernel "
+              "(not ported)", file=sys.stderr)
+        return EXIT_NOT_PORTED
     try:
         desc = problems.get_problem(args.problem)
     except KeyError as exc:

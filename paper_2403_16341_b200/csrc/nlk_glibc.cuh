@@ -1,3 +1,5 @@
+// SPDX-License-Identifier: LGPL-2.1-or-later AND BSD-3-Clause (see NOTICE):
+// glibc-derived libm ports (LGPL) and SVML-derived numpy exp/arctan (BSD-3).
 // Bit-exact device (and host) ports of the glibc 2.39 x86-64 FMA-variant
 // exp, pow (integer y), sin, cos and atan.
 //

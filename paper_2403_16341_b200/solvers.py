@@ -22,6 +22,7 @@ import torch
 
 from . import _lib
 from .core import (Problem, RetCode, SolveOptions, SolveResult, Stats, retcode_from_int)
+from .errors import IncompatibleSpec
 from .problems import DeviceResidual
 
 
@@ -118,13 +119,48 @@ def resolve_algorithm(algorithm):
         return ALGORITHM_PRESETS[algorithm]
     mod = type(algorithm).__module__ or ""
     if mod.startswith("nlkit"):
+        assemble(algorithm)  # IncompatibleSpec exactly where nlkit raises it
         import importlib
         nl_solvers = importlib.import_module(mod.rsplit(".", 1)[0] + ".solvers")
         for name, spec in nl_solvers.ALGORITHM_PRESETS.items():
             if spec == algorithm and name in ALGORITHM_PRESETS:
                 return ALGORITHM_PRESETS[name]
-        raise NotImplementedError(f"nlkit algorithm {algorithm!r} has no batched kernel")
+        raise NotImplementedError(f"nlkit algorithm {algorithm!r} is a valid specification "
+                                  "without a batched kernel")
     raise TypeError(f"cannot interpret {algorithm!r} as an algorithm")
+
+
+def assemble(spec):
+    """nlkit's block-compatibility validation (solvers.py:76-103), restated
+    on the attributes of an nlkit AlgorithmSpec: raises IncompatibleSpec with
+    the reference's message wherever ``nlkit.solvers.assemble`` would, so an
+    invalid specification fails the same way before any kernel is looked up
+    (run_algorithm calls it first, solvers.py:106-109)."""
+    jac, des, glob, lin = spec.jacobian, spec.descent, spec.globalization, spec.linear
+    materializes = jac.kind in ("analytic", "dual_dense", "fd_dense", "colored_sparse")
+    if jac.kind == "matrix_free" and lin.kind not in ("gmres", "auto"):
+        raise IncompatibleSpec("matrix-free Jacobians require an iterative "
+                               "Krylov linear solver (gmres or auto)")
+    if glob.kind == "trust_region":
+        if des.kind != "dogleg":
+            raise IncompatibleSpec("trust-region globalization requires the dogleg descent")
+        if not materializes:
+            raise IncompatibleSpec("trust region needs a materialized Jacobian "
+                                   "for the dogleg/steepest directions")
+    if des.kind == "dogleg" and glob.kind != "trust_region":
+        raise IncompatibleSpec("dogleg descent only runs inside a trust region")
+    if des.kind in ("halley", "potra_ptak") and glob.kind != "none":
+        raise IncompatibleSpec(f"{des.kind} manages its own steps; globalization must be none")
+    if jac.kind == "quasi_newton":
+        if des.kind != "newton":
+            raise IncompatibleSpec("quasi-Newton strategies provide only the "
+                                   "Newton-type inverse application")
+        if glob.kind == "trust_region":
+            raise IncompatibleSpec("quasi-Newton strategies cannot drive a "
+                                   "trust region (no explicit matrix)")
+    if des.kind in ("damped_newton", "steepest") and not materializes:
+        raise IncompatibleSpec(f"{des.kind} needs a materialized Jacobian")
+    return spec
 
 
 @dataclass

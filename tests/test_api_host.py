@@ -86,3 +86,45 @@ def test_result_json_roundtrip():
                          core.Stats(nf=3, njac=1, nlinsolve=1, nsteps=1))
     s = core.result_to_json(r)
     assert '"retcode": "Success"' in s and '"nf": 3' in s
+
+
+@pytest.mark.skipif(not os.path.isdir(NLKIT_SRC), reason="reference not present")
+def test_assemble_matches_reference():
+    """solvers.assemble raises IncompatibleSpec (same message) exactly where
+    nlkit.solvers.assemble does (solvers.py:76-103), over every combination
+    of Jacobian strategy x descent x globalization x linear solver; a valid
+    specification without a batched kernel is NotImplementedError, and the
+    presets map to their kernels."""
+    sys.path.insert(0, NLKIT_SRC)
+    import itertools
+
+    import nlkit
+    from nlkit import descent as nd, jacobians as nj, linalg as nl, quasinewton as nq
+    from nlkit import solvers as ns
+
+    from paper_2403_16341_b200.errors import IncompatibleSpec
+    jacs = [nj.ANALYTIC, nj.DUAL_DENSE, nj.FD_DENSE, nj.COLORED_SPARSE, nj.MATRIX_FREE,
+            nj.JacobianSpec("quasi_newton", qn=nq.QuasiNewtonConfig())]
+    descs = [nd.NEWTON, nd.STEEPEST, nd.DOGLEG, nd.HALLEY, nd.POTRA_PTAK, nd.DampedNewton()]
+    globs = [ns.NO_GLOBALIZATION, ns.LineSearch(), ns.TrustRegion()]
+    lins = [nl.AUTO, nl.LU, nl.QR, nl.GMRES()]
+    n_bad = 0
+    for j, d, g, li in itertools.product(jacs, descs, globs, lins):
+        spec = ns.AlgorithmSpec(jacobian=j, descent=d, globalization=g, linear=li)
+        try:
+            ns.assemble(spec)
+            ref = None
+        except nlkit.errors.IncompatibleSpec as e:
+            ref = str(e)
+        if ref is None:
+            assert solvers.assemble(spec) is spec
+        else:
+            n_bad += 1
+            with pytest.raises(IncompatibleSpec) as ei:
+                solvers.resolve_algorithm(spec)
+            assert str(ei.value) == ref
+    assert n_bad > 100
+    for name in ("newton-raphson", "trust-region", "broyden", "klement", "newton-backtracking"):
+        assert solvers.resolve_algorithm(ns.ALGORITHM_PRESETS[name]).name == name
+    with pytest.raises(NotImplementedError):
+        solvers.resolve_algorithm(ns.ALGORITHM_PRESETS["levenberg-marquardt"])

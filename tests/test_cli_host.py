@@ -42,3 +42,22 @@ def test_unknown_family_and_problem(capsys):  # test_cli.py:126-130, 46-50
                      "--algorithms", "newton-raphson"]) == 2
     assert cli.main(["solve", "nope", "newton-raphson"]) == 2
     assert "unknown" in capsys.readouterr().err
+
+
+def test_reference_only_presets_are_not_ported(capsys):
+    """A reference preset / problem with no batched kernel is reported as not
+    ported (exit 3), not as unknown (exit 2); names match nlkit's presets."""
+    import os
+    import sys
+    assert cli.main(["solve", "test23/rosenbrock", "levenberg-marquardt"]) == cli.EXIT_NOT_PORTED
+    assert "not ported" in capsys.readouterr().err
+    assert cli.main(["solve", "brusselator2d?N=8", "newton-raphson"]) == cli.EXIT_NOT_PORTED
+    assert cli.main(["solve", "test23/rosenbrock", "no-such-preset"]) == 2
+    src = os.environ.get("NLKIT_REF", "/root/reference/pkg/src")
+    if os.path.isdir(src):
+        sys.path.insert(0, src)
+        from nlkit import solvers as ns
+        from paper_2403_16341_b200 import solvers
+        ref = set(ns.list_algorithms())
+        ours = set(solvers.ALGORITHM_PRESETS) | {"polyalgorithm"}
+        assert set(cli.REFERENCE_ONLY_PRESETS) == ref - ours - {"dfsane"}
