@@ -361,6 +361,16 @@ def tasks_of(jobs):
             for pid, n, alg, b in jobs for i in range(len(b.u0))]
 
 
+def rank_rows(batch, global_batch, world, rank):
+    """Rows [lo, hi) of every job that this rank solves: a fixed global batch
+    split evenly (strong scaling, workloads.shard_bounds) or `batch` rows per
+    rank (weak scaling, rank r takes [r*batch, (r+1)*batch))."""
+    if global_batch:
+        from paper_2403_16341_b200.workloads import shard_bounds
+        return shard_bounds(global_batch, world, rank)
+    return rank * batch, (rank + 1) * batch
+
+
 def _hbm_peak():
     """HBM GB/s denominator: the driver-measured copy bandwidth of this pool
     (MEASURED_PEAKS.json), else the profiling recipe's stated fallback."""
@@ -381,11 +391,7 @@ def run_ours(args, rank, world, local_rank, dist):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     L = _lib.lib()
-    if args.global_batch:  # strong scaling: a fixed batch per job split N ways
-        from paper_2403_16341_b200.workloads import shard_bounds
-        lo, hi = shard_bounds(args.global_batch, world, rank)
-    else:  # weak scaling: B per job per GPU, rank r takes rows [rB, (r+1)B)
-        lo, hi = rank * args.batch, (rank + 1) * args.batch
+    lo, hi = rank_rows(args.batch, args.global_batch, world, rank)
     B = hi - lo
     f32 = args.dtype == "f32"
     tdt = torch.float32 if f32 else torch.float64

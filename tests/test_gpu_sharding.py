@@ -38,3 +38,21 @@ def test_sharded_devices_default_and_empty():
     assert got["u"].shape == (1000, 2) and (got["retcode"] == 0).all()
     with pytest.raises(ValueError):
         sharding.solve_batch_devices(b.problem_id, b.u0, b.p, "newton-raphson", devices=[], n=b.n)
+
+
+def test_sharded_c4_full_size():
+    """C4 as BASELINE.json states it: 10 M broyden-tridiagonal n = 16 systems,
+    SimpleDFSane, sharded over a device list (here the one GPU listed 4 and 8
+    times: the split and reassembly of the 2/4/8-GPU runs); every field of
+    every system equals the one-call solve."""
+    b = W.c4_tridiagonal(0, 10_000_000)
+    ref = solvers.solve_batch(b.problem_id, b.u0, None, "dfsane", n=16).to_numpy()
+    for devices in ([0] * 4, [0] * 8):
+        got = sharding.solve_batch_devices(b.problem_id, b.u0, None, "dfsane", devices=devices, n=16)
+        for k in sharding.FIELDS:
+            a, r = np.asarray(got[k]), np.asarray(ref[k])
+            if a.dtype.kind == "f":
+                assert np.array_equal(a.view(np.int64), r.view(np.int64)), k
+            else:
+                assert np.array_equal(a, r), k
+        del got
