@@ -403,7 +403,7 @@ def run_ours(args, rank, world, local_rank, dist):
     jobs = jobs_for(args.config, lo, hi)
     if args.only:
         keys = args.only.split(",")
-        jobs = [j for j in jobs if any(k in f"{j[0]}:{j[2]}" for k in keys)]
+        jobs = [j for j in jobs if any(k in f"{j[0]}:{j[2]}:n={j[1]}" for k in keys)]
 
     # device-resident SoA inputs (shared by the jobs of one problem) and outputs
     inputs, prepared = {}, []

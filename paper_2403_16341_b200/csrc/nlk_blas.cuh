@@ -14,6 +14,7 @@
 // All sizes are compile-time: loops unroll, arrays live in registers, and the
 // only data-dependent indices (pivots) are applied with predicated swaps.
 #pragma once
+#include "nlk_div.cuh"
 #include "nlk_dual.cuh"
 
 namespace nlk {

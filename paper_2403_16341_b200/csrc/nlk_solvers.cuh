@@ -645,7 +645,12 @@ struct QuasiNewton : Base<P, N, T, false> {
     T du[N];
     if constexpr (DIAG) {
 #pragma unroll
-      for (int i = 0; i < N; ++i) du[i] = -(B::f[i] / H[i]);
+      // ddiv: exact-root components make f_i (and below t_i) exactly zero,
+      // which nvcc's division sends to its slow path (nlk_div.cuh); measured
+      // C3 Klement n = 16 118 -> 77 ms, n = 8 52 -> 31 ms (profiles/r02m_*).
+      // Not used on the LU / trust-region / DFSane paths, where zero
+      // dividends are rare and the extra test on the serial chain cost 2-7 %.
+      for (int i = 0; i < N; ++i) du[i] = -ddiv(B::f[i], H[i]);
     } else {
       T Hf[N];
       gemv_A_x<N>(H, B::f, Hf);
@@ -698,7 +703,7 @@ struct QuasiNewton : Base<P, N, T, false> {
         T thresh = T(1e-9) * max_abs<N>(s);
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          if (fabs(s[i]) > thresh) H[i] = t[i] / s[i];
+          if (fabs(s[i]) > thresh) H[i] = ddiv(t[i], s[i]);
           if (fabs(H[i]) < T(1e-12)) H[i] = (H[i] >= T(0)) ? T(1e-12) : T(-1e-12);
         }
       } else {  // broyden_update (quasinewton.py:107-121)
@@ -711,7 +716,7 @@ struct QuasiNewton : Base<P, N, T, false> {
           for (int i = 0; i < N; ++i) {
             T a = s[i] - Ht[i];
 #pragma unroll
-            for (int j = 0; j < N; ++j) H[i + j * N] = H[i + j * N] + a * sH[j] / denom;
+            for (int j = 0; j < N; ++j) H[i + j * N] = H[i + j * N] + ddiv(a * sH[j], denom);
           }
         }
       }

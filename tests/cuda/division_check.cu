@@ -1,4 +1,5 @@
-// div_with_rcp(b, d, div_rcp(d)) against b / d, bit for bit (see nlk_div.cuh).
+// div_with_rcp(b, d, div_rcp(d)) and ddiv(b, d) against b / d, bit for bit
+// (see nlk_div.cuh).
 #include <cstdio>
 #include <cstdint>
 #include "nlk_div.cuh"
@@ -35,6 +36,14 @@ __global__ void hoisted(long long n, unsigned long long seed, double* out) {
     out[i] = nlk::div_with_rcp(b, d, nlk::div_rcp(d));
   }
 }
+__global__ void zerodiv(long long n, unsigned long long seed, double* out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t h1 = mix(seed + 2 * i), h2 = mix(seed + 2 * i + 1);
+    const double b = pick(mix(h1), static_cast<int>(h1 & 3)), d = pick(mix(h2), static_cast<int>((h1 >> 2) & 3));
+    out[i] = nlk::ddiv(b, d);
+  }
+}
 __global__ void plain(long long n, unsigned long long seed, double* out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -69,6 +78,8 @@ int main() {
     const unsigned long long seed = 12345 + 2ull * lo;
     hoisted<<<148 * 8, 256>>>(chunk, seed, x);
     plain<<<148 * 8, 256>>>(chunk, seed, y);
+    compare<<<148 * 8, 256>>>(chunk, seed, x, y, bad, ex);
+    zerodiv<<<148 * 8, 256>>>(chunk, seed, x);
     compare<<<148 * 8, 256>>>(chunk, seed, x, y, bad, ex);
   }
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("cuda error\n"); return 2; }

@@ -1,7 +1,8 @@
-"""The hoisted-reciprocal division of the shared-memory getrs
-(paper_2403_16341_b200/csrc/nlk_div.cuh) is bit-identical to nvcc's `b / d`
-on 10^8 random operands (any bit pattern, moderate and extreme exponents,
-zeros, subnormals, infinities, NaN)."""
+"""The divisions of paper_2403_16341_b200/csrc/nlk_div.cuh -- the
+hoisted-reciprocal division (div_with_rcp) and the zero-dividend shortcut
+used on the solve path (ddiv) -- are bit-identical to nvcc's `b / d` on 10^8
+random operands (any bit pattern, moderate and extreme exponents, zeros,
+subnormals, infinities, NaN)."""
 
 import os
 import subprocess
