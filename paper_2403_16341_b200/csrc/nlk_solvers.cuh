@@ -497,11 +497,13 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
     else dogleg_plain(out);
   }
   // one iteration of run_trust_region's loop (globalize.py:174-212).
-  // Measured and rejected (profiles/r02j_*, r02k_*): running the rejections
-  // up to the next acceptance inside one call (so the J + LU phases line up
-  // across a warp) -- trigonometric TR 64 -> 116 ms, matrix-sqrt-3x3 TR
-  // 161 -> 273 ms: lanes that accepted then wait for the longest rejection
-  // run of the warp.
+  // Measured and rejected (profiles/r02j_*, r02k_*, r02o_*): running the
+  // rejections up to the next acceptance inside one call (so the J + LU
+  // phases line up across a warp) -- trigonometric TR 64 -> 116 ms,
+  // matrix-sqrt-3x3 TR 161 -> 273 ms: lanes that accepted then wait for the
+  // longest rejection run of the warp; deferring a lane's J + LU (up to 2, 4
+  // or 8 trips) until half the warp needs one -- 62.5 -> 66.4 ms (the votes
+  // cost more than the alignment gains).
   NLK_FD int step(T abstol, int maxiters) {
     B::k += 1;
     if (!cached) {
