@@ -16,8 +16,21 @@ print('C2', round(d['value']/1e6,2), 'M/s', round(d['ms_per_step'],1), 'ms; e2e'
 bash tools/gpu_configs.sh ${T} c1 c3 c3f32 c4 c5 n16
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:solve_kernel --csv --log-file gpurun_out/${T}_launches.csv \
   python bench.py --steps 3 --warmup 0 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${T}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-bash tools/gpu_prof.sh ${T}_c2 c2 262144 "trigonometric:newton-raphson,matrix-sqrt-3x3:trust-region,trigonometric:trust-region"
-bash tools/gpu_prof.sh ${T}_c1 c1 16777216 "quadratic"
-bash tools/gpu_prof.sh ${T}_c3 c3 10000000 "klement:n=16"
-bash tools/gpu_prof.sh ${T}_c4 c4 10000000 "dfsane"
-bash tools/gpu_prof.sh ${T}_c5 c5 12500000 "dfsane"
+# ncu --set full captures, summarised on the box (reports are too large to ship back)
+prof() {  # name config batch only match bench-kernel-name
+  bash tools/gpu_prof.sh ${T}_$1 $2 $3 "$4"
+  python tools/ncu_summary.py gpurun_out/${T}_$1.ncu-rep > gpurun_out/${T}_ncu_$1.txt 2>&1
+  python tools/ncu_sass_hot.py gpurun_out/${T}_$1.ncu-rep 30 >> gpurun_out/${T}_ncu_$1.txt 2>&1
+  ncu -i gpurun_out/${T}_$1.ncu-rep --page source --csv --print-source cuda,sass > /tmp/${T}_$1_src.csv 2>/dev/null
+  python tools/ncu_source_split.py /tmp/${T}_$1_src.csv 30 >> gpurun_out/${T}_ncu_$1.txt 2>&1
+  NCU_JSON_DIR=gpurun_out python tools/ncu_pipe_json.py gpurun_out/${T}_$1.ncu-rep "$6" $3 "$5"
+  rm -f gpurun_out/${T}_$1.ncu-rep /tmp/${T}_$1_src.csv
+}
+prof c2nr c2 262144 "trigonometric:newton-raphson" "Trigonometric, 10, double, 0" "solve_kernel<test23/trigonometric,n=10,newton-raphson>"
+prof c2tr c2 262144 "trigonometric:trust-region" "Trigonometric, 10, double, 1" "solve_kernel<test23/trigonometric,n=10,trust-region>"
+prof c2ms c2 262144 "matrix-sqrt-3x3:trust-region" "MatrixSqrt3x3, 9, double, 1" "solve_kernel<test23/matrix-sqrt-3x3,n=9,trust-region>"
+prof c1 c1 16777216 "quadratic" "Quadratic<2>, 2, double, 0" "solve_kernel<quadratic,n=2,newton-raphson>"
+prof c3 c3 10000000 "klement:n=16" "GeneralizedRosenbrock<16>, 16, double, 3" "solve_kernel<generalized_rosenbrock,n=16,klement>"
+prof c4 c4 10000000 "dfsane" "BroydenTridiagonal<16>, 16, double, 4" "solve_kernel<test23/broyden-tridiagonal,n=16,dfsane>"
+prof c5 c5 12500000 "dfsane" "Quadratic<4>, 4, double, 4" "solve_kernel<quadratic,n=4,dfsane>"
+du -sh gpurun_out

@@ -25,8 +25,9 @@ def raw(rep):
 
 
 def main(args):
-    pj = os.path.join(ROOT, "profiles", "ncu_pipe.json")
-    tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    out = os.environ.get("NCU_JSON_DIR", os.path.join(ROOT, "profiles"))
+    pj = os.path.join(out, "ncu_pipe.json")
+    tj = os.path.join(out, "ncu_traffic.json")
     pipe = json.load(open(pj)) if os.path.exists(pj) else {}
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
     for rep, name, batch, match in zip(args[0::4], args[1::4], args[2::4], args[3::4]):
