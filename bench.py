@@ -361,6 +361,42 @@ def tasks_of(jobs):
             for pid, n, alg, b in jobs for i in range(len(b.u0))]
 
 
+def e2e_via_devices(args, prepared, dist, dev, total_systems, world):
+    """The e2e leg through the user-facing one-process sharder
+    (sharding.solve_batch_devices): each job's host batch (numpy [B, n]) is
+    split over the listed devices (--e2e-devices, e.g. "0,1,2,3"; under
+    torchrun each rank lists its own GPU), pinned, solved and gathered into
+    one host result buffer per job -- everything a user's call does, inside
+    the timed region."""
+    import torch
+    from paper_2403_16341_b200 import sharding
+    devices = [int(d) for d in args.e2e_devices.split(",")]
+    host = [(pid, n, alg, np.ascontiguousarray(b.u0), None if b.p is None else np.ascontiguousarray(b.p))
+            for pid, n, m, alg, h, u0, p, out, b in prepared]
+    f32 = args.dtype == "f32"
+
+    def step():
+        for pid, n, alg, u0, p in host:
+            sharding.solve_batch_devices(pid, u0, p, alg, devices=devices, n=n,
+                                         dtype=torch.float32 if f32 else torch.float64)
+
+    step()  # warm-up
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        step()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    esz = 4 if f32 else 8
+    bi = sum((u0.size + (0 if p is None else p.size)) * esz for _, _, _, u0, p in host)
+    bo = sum(len(u0) * ((n + 1) * esz + 1 + 16) for _, n, _, u0, _ in host)
+    return {"value": total_systems * args.e2e_steps / float(te.item()), "unit": "systems/s",
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": args.e2e_steps,
+            "api": f"sharding.solve_batch_devices(devices={devices}) per job, numpy in/out"}
+
+
 def rank_rows(batch, global_batch, world, rank):
     """Rows [lo, hi) of every job that this rank solves: a fixed global batch
     split evenly (strong scaling, workloads.shard_bounds) or `batch` rows per
@@ -507,7 +543,9 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # ---- e2e through the C-ABI with host buffers
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and args.e2e_devices:
+        e2e = e2e_via_devices(args, prepared, dist, dev, total_systems, world)
+    elif args.e2e_steps > 0:
         # a job is handed to the library as `pieces` contiguous column chunks
         # (each its own asynchronous call) when there are fewer jobs than
         # streams, so that the copies of one chunk overlap the solve of another
@@ -655,6 +693,9 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
                     help="arithmetic type (f32: registered fp32 instances, C1/C3/C4/C5)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-devices", default=None,
+                    help="e2e leg through sharding.solve_batch_devices over these devices "
+                         "(comma-separated ids; default: the C-ABI async host-buffer path)")
     ap.add_argument("--streams", type=int, default=1,
                     help="device-resident step: jobs round-robin over this many streams")
     ap.add_argument("--global-batch", type=int, default=None,

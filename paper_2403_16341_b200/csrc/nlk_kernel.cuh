@@ -227,7 +227,11 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   dev &= 63;
-  const size_t smem = sizeof(T) * kThreads * SolverOf<P, N, T, ALG>::type::kSmemElems;
+  size_t smem = sizeof(T) * kThreads * SolverOf<P, N, T, ALG>::type::kSmemElems;
+  // experiment knob: NLK_EXTRA_SMEM=<bytes> per block lowers the blocks per
+  // SM (occupancy sensitivity of a kernel; results are unchanged)
+  static const char* extra_smem = std::getenv("NLK_EXTRA_SMEM");
+  if (extra_smem) smem += std::atoi(extra_smem);
   if (per_sm_of[dev] == 0) {
     int sms = 0, per_sm = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
