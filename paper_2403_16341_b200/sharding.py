@@ -79,15 +79,16 @@ def solve_batch_devices(problem, u0, p=None, algorithm="newton-raphson", options
 
     ``u0`` [B, n] and ``p`` [B, m] are host arrays.  The batch is split into
     contiguous even slices (``shard_bounds``), one per entry of ``devices``
-    (default: every visible GPU; a device may repeat).  Each slice is copied
-    to pinned memory in SoA layout and handed to ``nlk_solve_batch_host_async``
-    on a stream of its own device -- staging H2D, the solve and the D2H of the
-    results, all asynchronous -- so the GPUs run side by side with no
-    inter-GPU traffic and every result lands in host memory.  Returns a dict
-    of host arrays with the fields of ``FIELDS`` for all B systems, in order.
+    (default: every visible GPU; a device may repeat).  Per slice, on a stream
+    of its own device and all asynchronous: the row-major slice is staged in
+    pinned memory and copied to the device as is, transposed to the kernels'
+    SoA layout there, solved (``nlk_solve_batch``), and every output is
+    transposed back on the device and copied straight into its rows of ONE
+    pinned host result per field -- no host-side transposes, no inter-GPU
+    traffic, no collective.  Returns a dict of host (numpy) arrays with the
+    fields of ``FIELDS`` for all B systems, in order; the arrays are views
+    of the pinned result buffers.
     """
-    import ctypes
-
     from . import _lib, solvers
     from .core import SolveOptions
 
@@ -116,43 +117,46 @@ def solve_batch_devices(problem, u0, p=None, algorithm="newton-raphson", options
         p = np.broadcast_to(p[None, :], (B, m)) if p.ndim == 1 else p
         if p.shape != (B, m):
             raise ValueError(f"p must be [{B}, {m}], got {p.shape}")
+        p = np.ascontiguousarray(p)
     if algorithm == "polyalgorithm" or algorithm is None:
         raise NotImplementedError("solve_batch_devices runs one algorithm; "
                                   "use solve_batch per device for the poly-algorithm")
     alg = solvers.resolve_algorithm(algorithm).kernel
-    L = _lib.lib()
-    code = 0 if dtype == torch.float64 else 1
-    jobs = []
+    # pinned staging of the inputs and pinned results, row-major as the caller's
+    hu0 = torch.empty((B, nn), dtype=dtype, pin_memory=True)
+    hu0.copy_(torch.from_numpy(u0))
+    hp = None
+    if m:
+        hp = torch.empty((B, m), dtype=dtype, pin_memory=True)
+        hp.copy_(torch.from_numpy(p))
+    res = {"u": torch.empty((B, nn), dtype=dtype, pin_memory=True),
+           "resid": torch.empty(B, dtype=dtype, pin_memory=True),
+           "retcode": torch.empty(B, dtype=torch.int8, pin_memory=True),
+           "counters": torch.empty((B, 4), dtype=torch.int32, pin_memory=True)}
+    streams = []
+    keep = []  # device tensors alive until their stream is synchronised
     for r, dev in enumerate(devices):
         lo, hi = shard_bounds(B, len(devices), r)
         if hi <= lo:
             continue
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        hu0 = pin(u0[lo:hi].T)
-        hp = pin(p[lo:hi].T) if m else None
-        k = hi - lo
-        out = {"u": torch.empty((nn, k), dtype=dtype).pin_memory(),
-               "resid": torch.empty(k, dtype=dtype).pin_memory(),
-               "retcode": torch.empty(k, dtype=torch.int8).pin_memory(),
-               "counters": torch.empty((4, k), dtype=torch.int32).pin_memory()}
-        with torch.cuda.device(dev):
-            st = torch.cuda.Stream(dev)
-            c = out["counters"]
-            _lib.check(L.nlk_solve_batch_host_async(
-                handle, alg, code, k, hu0.data_ptr(), None if hp is None else hp.data_ptr(),
-                float(options.abstol), int(options.maxiters), out["u"].data_ptr(),
-                out["resid"].data_ptr(), out["retcode"].data_ptr(), c[0].data_ptr(),
-                c[1].data_ptr(), c[2].data_ptr(), c[3].data_ptr(), ctypes.c_void_p(st.cuda_stream)))
-        jobs.append((lo, hi, st, out, hu0, hp))
-    res = {"u": np.empty((B, nn), dtype=npdt), "resid": np.empty(B, dtype=npdt),
-           "retcode": np.empty(B, dtype=np.int8)}
-    for f in ("nsteps", "nf", "njac", "nlinsolve"):
-        res[f] = np.empty(B, dtype=np.int32)
-    for lo, hi, st, out, _hu0, _hp in jobs:
+        d = torch.device("cuda", dev)
+        with torch.cuda.device(d):
+            st = torch.cuda.Stream(d)
+            with torch.cuda.stream(st):
+                du0 = hu0[lo:hi].to(d, non_blocking=True).t().contiguous()
+                dp = None if hp is None else hp[lo:hi].to(d, non_blocking=True).t().contiguous()
+                out = solvers.solve_batch_soa(handle, alg, du0, dp, options.abstol,
+                                              options.maxiters, stream=st.cuda_stream)
+                res["u"][lo:hi].copy_(out["u"].t().contiguous(), non_blocking=True)
+                res["resid"][lo:hi].copy_(out["resid"], non_blocking=True)
+                res["retcode"][lo:hi].copy_(out["retcode"], non_blocking=True)
+                res["counters"][lo:hi].copy_(out["counters"].t().contiguous(), non_blocking=True)
+        streams.append(st)
+        keep.append((du0, dp, out))
+    for st in streams:
         st.synchronize()
-        res["u"][lo:hi] = out["u"].numpy().T
-        res["resid"][lo:hi] = out["resid"].numpy()
-        res["retcode"][lo:hi] = out["retcode"].numpy()
-        for j, f in enumerate(("nsteps", "nf", "njac", "nlinsolve")):
-            res[f][lo:hi] = out["counters"][j].numpy()
-    return res
+    del keep
+    c = res["counters"].numpy()
+    return {"u": res["u"].numpy(), "resid": res["resid"].numpy(),
+            "retcode": res["retcode"].numpy(), "nsteps": c[:, 0], "nf": c[:, 1],
+            "njac": c[:, 2], "nlinsolve": c[:, 3]}
