@@ -716,6 +716,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional test of the N > 1 path on a one-GPU box (tests/ and DESIGN §5):
+    # NLK_BENCH_DEVICE pins every rank to one device, NLK_BENCH_BACKEND=gloo
+    # replaces NCCL (which refuses two ranks on one GPU).  Never a measurement.
+    if os.environ.get("NLK_BENCH_DEVICE") is not None:
+        local_rank = int(os.environ["NLK_BENCH_DEVICE"])
 
     if args.impl == "reference":
         if rank != 0:
@@ -753,7 +758,11 @@ def main():
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("NLK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
     result, stats, jobs = run_ours(args, rank, world, local_rank, dist)
     if rank == 0:
