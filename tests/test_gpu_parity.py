@@ -58,14 +58,17 @@ def test_golden(case):
     check_against(g, got, case["case"], case["problem_id"])
 
 
+@pytest.mark.parametrize("sigma", [0.1, 1.0])
 @pytest.mark.parametrize("alg", ["newton-raphson", "trust-region"])
 @pytest.mark.parametrize("index", range(1, 24))
-def test_oracle_c2_sample(index, alg):
+def test_oracle_c2_sample(index, alg, sigma):
+    """C2's 20k-system samples at the primary sigma = 0.1 and the stress
+    sigma = 1.0."""
     from oracle import oracle as O
-    b = W.c2_suite(index, 0, 20000, 0.1)
+    b = W.c2_suite(index, 0, 20000, sigma)
     ref = O.solve_batch(b.problem_id, alg, b.u0)
     got = gpu_solve(b.problem_id, alg, b.u0)
-    check_against(ref, got, f"C2 #{index} {alg}", b.problem_id)
+    check_against(ref, got, f"C2 #{index} {alg} sigma={sigma}", b.problem_id)
 
 
 @pytest.mark.parametrize("alg", ["broyden", "klement", "dfsane", "newton-raphson", "trust-region"])
