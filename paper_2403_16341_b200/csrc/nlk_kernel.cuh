@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solv
 }
 
 // Static schedule for problem families whose iteration counts are tight
-// (P::kStaticSchedule, e.g. the parametrised quadratic of C1/C5: 4-8 Newton
+// (P::kStaticAlgs, e.g. the parametrised quadratic of C1/C5: 4-8 Newton
 // steps on every system).  Each thread takes systems by grid stride and runs
 // each to completion: a warp's lanes always hold consecutive systems, so
 // every load and store of the SoA batch is one coalesced transaction, and
@@ -207,15 +207,16 @@ __global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solv
 #ifndef NLK_SCHEDULE_STATIC
 #define NLK_SCHEDULE_STATIC 1
 #endif
-template <class P> struct UseStatic {
-  static constexpr bool value = NLK_SCHEDULE_STATIC_ALL || (NLK_SCHEDULE_STATIC && StaticSchedule<P>::value);
+template <class P, int ALG> struct UseStatic {
+  static constexpr bool value =
+      NLK_SCHEDULE_STATIC_ALL || (NLK_SCHEDULE_STATIC && StaticSchedule<P, ALG>::value);
 };
 
 // Host-side launcher: persistent grid sized from the occupancy calculator.
 template <class P, int N, class T, int ALG>
 cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out) {
   auto kern = [] {
-    if constexpr (UseStatic<P>::value) return solve_kernel_static<P, N, T, ALG>;
+    if constexpr (UseStatic<P, ALG>::value) return solve_kernel_static<P, N, T, ALG>;
     else return solve_kernel<P, N, T, ALG>;
   }();
   constexpr int kThreads = block_of<P, N, T, ALG>();

@@ -195,11 +195,20 @@ struct JacRankOneDiag<P, std::void_t<decltype(P::kJacRankOneDiag)>> {
 };
 // Problems whose iteration counts are tight run on the static (grid-stride)
 // schedule of nlk_kernel.cuh instead of the refilling one
-template <class P, class = void> struct StaticSchedule { static constexpr bool value = false; };
+// P::kStaticAlgs: bit a set = algorithm a (nlk_solvers.cuh Alg: 0 NR, 1 TR,
+// 2 Broyden, 3 Klement, 4 DFSane, 5 NR + line search) runs the static schedule
+template <class P, class = void> struct StaticAlgs { static constexpr int value = 0; };
 template <class P>
-struct StaticSchedule<P, std::void_t<decltype(P::kStaticSchedule)>> {
-  static constexpr bool value = P::kStaticSchedule;
+struct StaticAlgs<P, std::void_t<decltype(P::kStaticAlgs)>> {
+  static constexpr int value = P::kStaticAlgs;
 };
+template <class P, int ALG> struct StaticSchedule {
+  static constexpr bool value = (StaticAlgs<P>::value >> ALG) & 1;
+};
+// Newton, trust region and Newton + line search (kStaticNewtonTR): suite
+// problems whose iteration counts stay tight over C2's perturbed starts, at
+// sigma = 0.1 and at the stress sigma = 1.0 (max 32 steps)
+constexpr int kStaticNewtonTR = (1 << 0) | (1 << 1) | (1 << 5);
 template <class P, class = void> struct MemoOf { static constexpr int value = 0; };
 template <class P> struct MemoOf<P, std::void_t<decltype(P::kMemo)>> { static constexpr int value = P::kMemo; };
 
@@ -212,6 +221,7 @@ struct Rosenbrock {  // 36-40
   }
 };
 struct PowellSingular {  // 43-49
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 4, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] + K(10.0) * x[1];
@@ -237,6 +247,7 @@ struct Wood {  // 59-67
   }
 };
 struct HelicalValley {  // 70-81
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 3, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     const T twopi = K(6.283185307179586);  // 2.0 * math.pi
@@ -255,6 +266,7 @@ struct HelicalValley {  // 70-81
   }
 };
 struct Watson {  // 84-109 (n = 2)
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 2, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll 1
@@ -287,6 +299,7 @@ struct Watson {  // 84-109 (n = 2)
   }
 };
 struct Chebyquad {  // 112-129 (n = 2)
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 2, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
@@ -319,6 +332,7 @@ struct BrownAlmostLinear {  // 132-139
   }
 };
 struct DiscreteBoundaryValue {  // 142-151
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 10, M = 0;
   static constexpr int kMemo = N;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
@@ -334,6 +348,7 @@ struct DiscreteBoundaryValue {  // 142-151
   }
 };
 struct DiscreteIntegral {  // 154-168
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 10, M = 0;
   static constexpr int kMemo = N;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
@@ -412,6 +427,7 @@ struct Trigonometric {  // 171-177
   }
 };
 struct VariablyDimensioned {  // 180-188
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 10, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S w[N];
@@ -425,6 +441,7 @@ struct VariablyDimensioned {  // 180-188
 };
 template <int NN>
 struct BroydenTridiagonal {  // 191-198 (n-generic)
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = NN, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
@@ -437,6 +454,7 @@ struct BroydenTridiagonal {  // 191-198 (n-generic)
   }
 };
 struct BroydenBanded {  // 201-210
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 10, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
 #pragma unroll
@@ -562,6 +580,7 @@ struct ProductExponential {  // 240-251
   }
 };
 struct CubicRadial {  // 254-260
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 2, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     S r2 = x[0] * x[0] + x[1] * x[1];
@@ -570,6 +589,7 @@ struct CubicRadial {  // 254-260
   }
 };
 struct DoubleRootScalar {  // 263-266
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 1, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     out[0] = x[0] * t_pow2(x[0] - K(5.0));
@@ -591,6 +611,7 @@ struct Boggs {  // 276-280
   }
 };
 struct Chandrasekhar {  // 286-292
+  static constexpr int kStaticAlgs = kStaticNewtonTR;
   static constexpr int N = 10, M = 0;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T*, S* out, C& cx) {
     T mu[N];
@@ -631,8 +652,8 @@ struct GeneralizedRosenbrock {  // 363-368
 template <int NN>
 struct Quadratic {  // 382-383: u * u - theta
   static constexpr int N = NN, M = NN;
-  // C1/C5 iteration counts are tight (4-8 steps): grid-stride schedule
-  static constexpr bool kStaticSchedule = true;
+  // C1/C5 iteration counts are tight (4-8 steps): grid-stride schedule, every solver
+  static constexpr int kStaticAlgs = 0x3f;
   template <class S, class T, class C> NLK_FD static void f(const S* x, const T* p, S* out, C& cx) {
 #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = x[i] * x[i] - p[i];

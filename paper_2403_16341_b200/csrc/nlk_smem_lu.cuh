@@ -30,10 +30,6 @@ namespace nlk {
 #ifndef NLK_SMEM_TR_MIN
 #define NLK_SMEM_TR_MIN 2
 #endif
-// the same threshold for the statically scheduled families (quadratic)
-#ifndef NLK_SMEM_STATIC_MIN
-#define NLK_SMEM_STATIC_MIN 2
-#endif
 // 1: unroll every loop (immediate smem offsets); 0: rolled loops
 #ifndef NLK_SMEM_UNROLL
 #define NLK_SMEM_UNROLL 1

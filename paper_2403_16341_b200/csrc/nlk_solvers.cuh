@@ -237,7 +237,7 @@ struct Base {
 template <class P, int N, class T, bool LS>
 struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
   using B = Base<P, N, T, true, NLK_SINCOS_PAIRS_NR>;
-  using SL = UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_NR_MIN>;
+  using SL = UseSmemLU<N, T, NLK_SMEM_NR_MIN>;
   static constexpr bool SM = SL::value;
   static constexpr int kSmemElems = SM ? N * N + N : 0;
   static constexpr int kStride = SM ? SL::stride : kSmStride;
@@ -326,7 +326,7 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 template <class P, int N, class T>
 struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR>;
-  using SL = UseSmemLU<N, T, StaticSchedule<P>::value ? NLK_SMEM_STATIC_MIN : NLK_SMEM_TR_MIN>;
+  using SL = UseSmemLU<N, T, NLK_SMEM_TR_MIN>;
   static constexpr bool SM = SL::value;
   static constexpr int kStride = SM ? SL::stride : kSmStride;
   using Mat = SMat<N, T, kStride>;
