@@ -614,6 +614,23 @@ template <class P, int N, class T, bool DIAG>
 struct QuasiNewton : Base<P, N, T, false> {
   using B = Base<P, N, T, false>;
   T H[DIAG ? N : N * N];  // inverse Jacobian (column-major) or Jacobian diagonal
+  // Broyden: H is kept implicit while it is the identity (IDENTITY_INIT and
+  // every reinit) and only written out at the first update.  dgemv with the
+  // identity (gemv_A_x / gemv_AT_x: accumulators start at +0, N >= 4) returns
+  // x_i for x_i != 0 and +0 for x_i = +-0 (every other term is a +-0 product
+  // of a finite x; x is finite wherever H is applied), so
+  // idgemv(x)_i = (x_i == 0 ? +0 : x_i) is the same bits without the 2 N^2
+  // loads of H.  (N < 4: the dgemv tails can return -0; H stays explicit.
+  // An update with a non-finite s or t writes H out first: 0 * inf is NaN.)
+#ifndef NLK_QN_LAZY_ID
+#define NLK_QN_LAZY_ID 1
+#endif
+  static constexpr bool LAZY = !DIAG && NLK_QN_LAZY_ID && N >= 4;
+  bool hid;
+  NLK_FD static void idgemv(const T* x, T* y) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[i] = (x[i] == T(0)) ? T(0) : x[i];
+  }
   int reinits, since;
   // stalling window (Klement): min of hist[:-3] and the last three entries
   T prev_min, last[3];
@@ -623,10 +640,15 @@ struct QuasiNewton : Base<P, N, T, false> {
     if constexpr (DIAG) {
 #pragma unroll
       for (int i = 0; i < N; ++i) H[i] = T(1);
+    } else if constexpr (LAZY) {
+      hid = true;
     } else {
-#pragma unroll
-      for (int i = 0; i < N * N; ++i) H[i] = (i % N == i / N) ? T(1) : T(0);
+      id_write();
     }
+  }
+  NLK_FD void id_write() {
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) H[i] = (i % N == i / N) ? T(1) : T(0);
   }
   NLK_FD void hist_reset(T v) { hlen = 1; last[2] = v; prev_min = T(INFINITY); }
   NLK_FD void hist_push(T v) {
@@ -655,7 +677,8 @@ struct QuasiNewton : Base<P, N, T, false> {
       for (int i = 0; i < N; ++i) du[i] = -ddiv(B::f[i], H[i]);
     } else {
       T Hf[N];
-      gemv_A_x<N>(H, B::f, Hf);
+      if (LAZY && hid) idgemv(B::f, Hf);
+      else gemv_A_x<N>(H, B::f, Hf);
 #pragma unroll
       for (int i = 0; i < N; ++i) du[i] = -Hf[i];
     }
@@ -710,10 +733,24 @@ struct QuasiNewton : Base<P, N, T, false> {
         }
       } else {  // broyden_update (quasinewton.py:107-121)
         T Ht[N], sH[N];
-        gemv_A_x<N>(H, t, Ht);
-        gemv_AT_x<N>(H, s, sH);
+        // s = un - u and t = fn - f can overflow: 0 * inf is NaN in dgemv
+        if (LAZY && hid && !(all_finite<N>(s) && all_finite<N>(t))) {
+          id_write();
+          hid = false;
+        }
+        if (LAZY && hid) {
+          idgemv(t, Ht);
+          idgemv(s, sH);
+        } else {
+          gemv_A_x<N>(H, t, Ht);
+          gemv_AT_x<N>(H, s, sH);
+        }
         T denom = ddot<N>(s, Ht);
         if (!(fabs(denom) < T(1e-12) * norm2<N>(s) * norm2<N>(Ht))) {
+          if (LAZY && hid) {
+            id_write();
+            hid = false;
+          }
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             T a = s[i] - Ht[i];

@@ -147,3 +147,36 @@ def test_brown_almost_linear_closed_form_edges_match_oracle():
         for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
             assert np.array_equal(got[f], ref[f]), (alg, f)
         assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"]), alg
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_broyden_implicit_identity_edges_match_oracle(n):
+    """Broyden keeps H implicit while it is the identity (nlk_solvers.cuh,
+    QuasiNewton::LAZY): residual components that are exactly +0 / -0 (the
+    identity dgemv's zero signs), exact-zero and huge starts (updates with
+    overflowing s / t write H out first), bit-identical to the oracle."""
+    rng = np.random.default_rng(40 + n)
+    B = 4096
+    # generalized Rosenbrock: f_i = 10 (x_i - x_{i-1}^2) is -0 for x_i = -0, x_{i-1} = +-0
+    u0 = rng.uniform(-2.0, 2.0, (B, n)) * 10.0 ** rng.integers(-3, 4, (B, 1))
+    for i in range(B):
+        if i % 3 == 0:
+            k = rng.integers(1, n)
+            u0[i, k - 1], u0[i, k] = rng.choice([0.0, -0.0]), -0.0
+        if i % 7 == 0:
+            u0[i, rng.integers(n)] = rng.choice([1e150, -1e150, 1e300, 0.0])
+    got = _solve("generalized_rosenbrock", "broyden", u0, None, 1e-8, 1000)
+    ref = O.solve_batch("generalized_rosenbrock", "broyden", u0, None)
+    for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        assert np.array_equal(got[f], ref[f]), f
+    assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"])
+    # quadratic: p_i = u0_i^2 makes f_i exactly +0 at the start
+    u0 = rng.uniform(0.1, 3.0, (B, n)) * rng.choice([-1.0, 1.0], (B, n))
+    p = rng.uniform(0.5, 10.0, (B, n)) ** 2
+    mask = rng.random((B, n)) < 0.3
+    p[mask] = u0[mask] * u0[mask]
+    got = _solve("quadratic", "broyden", u0, p, 1e-8, 1000)
+    ref = O.solve_batch("quadratic", "broyden", u0, p)
+    for f in ("retcode", "nsteps", "nf", "njac", "nlinsolve"):
+        assert np.array_equal(got[f], ref[f]), f
+    assert _same(got["u"], ref["u"]) and _same(got["resid"], ref["resid"])
