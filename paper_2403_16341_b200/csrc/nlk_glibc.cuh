@@ -223,14 +223,47 @@ constexpr double kS5 = -0x1.addffc2fcdf59p-26, kS4 = 0x1.71de27b9a7ed9p-19;
 constexpr double kS3 = -0x1.a01a019db08b8p-13, kS2 = 0x1.1111111110ecep-7;
 constexpr double kS1 = -0x1.5555555555555p-3, kSmall = 0.126;
 
+// NLK_GLIBC_CBANK: device code reads these constants from the constant bank
+// (c[..] operands) instead of materialising each 64-bit value with two moves
+// per use inside the out-of-line sincos calls.  Same values, same operations.
+#ifndef NLK_GLIBC_CBANK
+#define NLK_GLIBC_CBANK 1
+#endif
+#if defined(__CUDACC__) && NLK_GLIBC_CBANK
+static __constant__ double cb_kBig = kBig;
+static __constant__ double cb_kSn5 = kSn5;
+static __constant__ double cb_kSn3 = kSn3;
+static __constant__ double cb_kCs6 = kCs6;
+static __constant__ double cb_kCs4 = kCs4;
+static __constant__ double cb_kCs2 = kCs2;
+static __constant__ double cb_kHp0 = kHp0;
+static __constant__ double cb_kHp1 = kHp1;
+static __constant__ double cb_kToint = kToint;
+static __constant__ double cb_kHpinv = kHpinv;
+static __constant__ double cb_kMp1 = kMp1;
+static __constant__ double cb_kMp2 = kMp2;
+static __constant__ double cb_kPp3 = kPp3;
+static __constant__ double cb_kPp4 = kPp4;
+static __constant__ double cb_kS5 = kS5;
+static __constant__ double cb_kS4 = kS4;
+static __constant__ double cb_kS3 = kS3;
+static __constant__ double cb_kS2 = kS2;
+static __constant__ double cb_kS1 = kS1;
+static __constant__ double cb_kSmall = kSmall;
+#endif
+#if defined(__CUDA_ARCH__) && NLK_GLIBC_CBANK
+#define K_(name) cb_##name
+#else
+#define K_(name) name
+#endif
 NLK_HD double sct(int i) { return asd(NLK_PICK(sincos_tab, i)); }
 
 NLK_HD double taylor_sin(double a, double da) {
   const double xx = a * a;
-  double p = dfma(xx, kS5, kS4);
-  p = dfma(xx, p, kS3);
-  p = dfma(xx, p, kS2);
-  p = dfma(xx, p, kS1);
+  double p = dfma(xx, K_(kS5), K_(kS4));
+  p = dfma(xx, p, K_(kS3));
+  p = dfma(xx, p, K_(kS2));
+  p = dfma(xx, p, K_(kS1));
   double t = dfma(p, a, -(da * 0.5));
   t = dfma(xx, t, da);
   return a + t;
@@ -238,14 +271,14 @@ NLK_HD double taylor_sin(double a, double da) {
 NLK_HD double do_sin_tab(double a, double da) {
   if (!(0.0 < a)) da = -da;
   const double ax = fabs(a);
-  const double u = ax + kBig;
+  const double u = ax + K_(kBig);
   const int k = static_cast<int>(static_cast<uint32_t>(asu(u)) << 2);
-  const double xr = ax - (u - kBig);
+  const double xr = ax - (u - K_(kBig));
   const double xx = xr * xr;
-  const double a5 = dfma(xx, kSn5, kSn3);
+  const double a5 = dfma(xx, K_(kSn5), K_(kSn3));
   double s = dfma(xr * xx, a5, da);
-  double c = dfma(xx, kCs6, kCs4);
-  c = dfma(xx, c, kCs2);
+  double c = dfma(xx, K_(kCs6), K_(kCs4));
+  c = dfma(xx, c, K_(kCs2));
   s = xr + s;
   const double cc = xx * c;
   c = dfma(xr, da, cc);
@@ -257,14 +290,14 @@ NLK_HD double do_sin_tab(double a, double da) {
 NLK_HD double do_cos_tab(double a, double da) {
   if (a < 0.0) da = -da;
   const double ax = fabs(a);
-  const double u = ax + kBig;
+  const double u = ax + K_(kBig);
   const int k = static_cast<int>(static_cast<uint32_t>(asu(u)) << 2);
-  const double xr = (ax - (u - kBig)) + da;
+  const double xr = (ax - (u - K_(kBig))) + da;
   const double xx = xr * xr;
-  const double a5 = dfma(xx, kSn5, kSn3);
+  const double a5 = dfma(xx, K_(kSn5), K_(kSn3));
   const double s = dfma(xr * xx, a5, xr);
-  double c = dfma(xx, kCs6, kCs4);
-  c = dfma(xx, c, kCs2);
+  double c = dfma(xx, K_(kCs6), K_(kCs4));
+  c = dfma(xx, c, K_(kCs2));
   const double cc = xx * c;
   double t = dfma(-s, sct(k + 1), sct(k + 3));
   t = dfma(-cc, sct(k + 2), t);
@@ -272,19 +305,19 @@ NLK_HD double do_cos_tab(double a, double da) {
   return sct(k + 2) + t;
 }
 NLK_HD double do_sin(double a, double da) {
-  if (fabs(a) < kSmall) return taylor_sin(a, da);
+  if (fabs(a) < K_(kSmall)) return taylor_sin(a, da);
   return do_sin_tab(a, da);
 }
 NLK_HD int reduce_sincos(double x, double* a, double* da) {
-  const double t = dfma(x, kHpinv, kToint);
+  const double t = dfma(x, K_(kHpinv), K_(kToint));
   const int n = static_cast<int>(static_cast<uint32_t>(asu(t)) & 3);
-  const double xn = t - kToint;
-  double y = dfma(-xn, kMp1, x);
-  y = dfma(-xn, kMp2, y);
-  const double t2 = dfma(-xn, kPp3, y);
-  const double db = dfma(-xn, kPp3, y - t2);
-  const double b = dfma(-xn, kPp4, t2);
-  const double e = dfma(-xn, kPp4, t2 - b);
+  const double xn = t - K_(kToint);
+  double y = dfma(-xn, K_(kMp1), x);
+  y = dfma(-xn, K_(kMp2), y);
+  const double t2 = dfma(-xn, K_(kPp3), y);
+  const double db = dfma(-xn, K_(kPp3), y - t2);
+  const double b = dfma(-xn, K_(kPp4), t2);
+  const double e = dfma(-xn, K_(kPp4), t2 - b);
   *a = b;
   *da = db + e;
   return n;
@@ -479,16 +512,16 @@ NLK_HD bool sincos_n(const double* x, double* s, double* c) {
     const double xs = big ? 0.5 : x[g];  // keeps every table index in range
     double a, da;
     const int nn = reduce_sincos(xs, &a, &da);
-    const double y = kHp0 - fabs(xs);
-    const double a1 = y + kHp1;
-    const double da1 = (y - a1) + kHp1;
+    const double y = K_(kHp0) - fabs(xs);
+    const double a1 = y + K_(kHp1);
+    const double da1 = (y - a1) + K_(kHp1);
     const int m = (k < 0x3feb6000u) ? 0 : ((k < 0x400368fdu) ? 1 : 2);
     mode[g] = m;
     n[g] = nn;
     as[g] = m == 0 ? xs : (m == 1 ? a1 : a);
     das[g] = m == 0 ? 0.0 : (m == 1 ? da1 : da);
     ac[g] = m == 0 ? xs : (m == 1 ? y : a);
-    dac[g] = m == 0 ? 0.0 : (m == 1 ? kHp1 : da);
+    dac[g] = m == 0 ? 0.0 : (m == 1 ? K_(kHp1) : da);
   }
 #if defined(__CUDA_ARCH__)
 #pragma unroll
@@ -496,7 +529,7 @@ NLK_HD bool sincos_n(const double* x, double* s, double* c) {
   for (int g = 0; g < G; ++g) {
     const double vt = taylor_sin(as[g], das[g]);
     const double vb = do_sin_tab(as[g], das[g]);
-    const double vs = (fabs(as[g]) < kSmall) ? vt : vb;
+    const double vs = (fabs(as[g]) < K_(kSmall)) ? vt : vb;
     const double vc = do_cos_tab(ac[g], dac[g]);
     const uint32_t k = static_cast<uint32_t>(asu(x[g]) >> 32) & 0x7fffffffu;
     const int nn = n[g];
@@ -511,6 +544,8 @@ NLK_HD bool sincos_n(const double* x, double* s, double* c) {
   }
   return slow;
 }
+
+#undef K_
 
 // ---- atan (sysdeps/ieee754/dbl-64/s_atan.c, 2.35+ table version, FMA build) --
 constexpr double kA0 = 0x1.375f08b31cbcep-4, kA1 = -0x1.7458022b13c25p-4;

@@ -299,11 +299,14 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 #pragma unroll
     for (int i = 0; i < N; ++i) un[i] = B::u[i] + alpha * du[i];
     B::F(un, fn);
-    if (!(all_finite<N>(un) && all_finite<N>(fn))) return NONFINITE;
+    // one max|fn| for both tests: it is finite iff every fn_i is (max_abs
+    // propagates NaN), and converged(fn) is isfinite(m) && m <= abstol
+    const T mf = max_abs<N>(fn);
+    if (!(all_finite<N>(un) && isfinite(mf))) return NONFINITE;
 #pragma unroll
     for (int i = 0; i < N; ++i) { B::u[i] = un[i]; B::f[i] = fn[i]; }
     B::nsteps += 1;
-    if (converged<N>(B::f, abstol)) return SUCCESS;
+    if (mf <= abstol) return SUCCESS;
     return B::k >= maxiters ? MAXITERS : RUNNING;
   }
 };
@@ -687,7 +690,8 @@ struct QuasiNewton : Base<P, N, T, false> {
 #pragma unroll
     for (int i = 0; i < N; ++i) un[i] = B::u[i] + T(1) * du[i];
     B::F(un, fn);
-    if (!(all_finite<N>(un) && all_finite<N>(fn))) return NONFINITE;
+    const T mf = max_abs<N>(fn);  // as in NewtonRaphson::step
+    if (!(all_finite<N>(un) && isfinite(mf))) return NONFINITE;
     T nnew = norm2<N>(fn);
     bool merit_decreased = nnew < norm2<N>(B::f);
     T s[N], t[N];
@@ -700,7 +704,7 @@ struct QuasiNewton : Base<P, N, T, false> {
     }
     B::nsteps += 1;
     if constexpr (DIAG) hist_push(nnew);
-    if (converged<N>(B::f, abstol)) return SUCCESS;
+    if (mf <= abstol) return SUCCESS;
     bool reinit;
     if constexpr (!DIAG) {  // NOT_DESCENT (quasinewton.py:188-193)
       T mdu = max_abs<N>(du);
@@ -816,7 +820,8 @@ struct DFSane : Base<P, N, T, false> {
       lo = T(0.1) * am; hi = T(0.5) * am;
       am = !(tm > lo) ? lo : (tm > hi ? hi : tm);
     }
-    if (!(all_finite<N>(ua) && all_finite<N>(fa))) return NONFINITE;
+    const T mf = max_abs<N>(fa);  // as in NewtonRaphson::step
+    if (!(all_finite<N>(ua) && isfinite(mf))) return NONFINITE;
     T s[N], y[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -831,7 +836,7 @@ struct DFSane : Base<P, N, T, false> {
 #pragma unroll
     for (int i = 0; i < MEM; ++i)
       if (i == slot) hist[i] = fnorm;
-    if (converged<N>(B::f, abstol)) return SUCCESS;
+    if (mf <= abstol) return SUCCESS;
     T ss = ddot<N>(s, s);
     T sy = ddot<N>(s, y);
     sigma = ss / sy;
