@@ -102,8 +102,11 @@ template <int N, class S> NLK_FD S np_prod(const S* x) {
 #ifndef NLK_SINCOS_PAIRS_NR
 #define NLK_SINCOS_PAIRS_NR 1
 #endif
+// (the trust region too since round 2: trig TR 63.3 -> 61.1 ms; in round 1,
+// before the compressed Jacobian and the dogleg cache, its extra live state
+// spilled and pairs measured slower there)
 #ifndef NLK_SINCOS_PAIRS_TR
-#define NLK_SINCOS_PAIRS_TR 0
+#define NLK_SINCOS_PAIRS_TR 1
 #endif
 template <class T, int MODE, bool SCPAIRS = false>
 struct Ctx {

@@ -45,8 +45,10 @@ namespace nlk {
 #define NLK_GETRS_HOIST_DIV 0
 #endif
 // 1: getrs substitutes on a register copy of the permuted right-hand side
+// (round 2: msqrt-3x3 TR 161.2 -> 159.0 ms, trig TR 60.9 -> 60.6; neutral in
+// round 1)
 #ifndef NLK_GETRS_REG
-#define NLK_GETRS_REG 0
+#define NLK_GETRS_REG 1
 #endif
 
 #define NLK_FD __device__ __forceinline__
