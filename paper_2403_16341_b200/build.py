@@ -46,13 +46,14 @@ def _newest_header():
     return max(os.path.getmtime(h) for h in hs) if hs else 0.0
 
 
-def _compile(src, force, verbose, obj_dir=OBJ, defines=()):
+def _compile(src, force, verbose, obj_dir=OBJ, defines=(), xptxas=()):
     obj = os.path.join(obj_dir, os.path.basename(src).replace(".cu", ".o"))
     log = obj.replace(".o", ".ptxas.log")
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), _newest_header())):
         return obj, None
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *source_flags(src), *[f"-D{d}" for d in defines],
+           *[a for x in xptxas for a in ("-Xptxas", x)], "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,6 +62,17 @@ def _compile(src, force, verbose, obj_dir=OBJ, defines=()):
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr[-4000:]}")
     return obj, log
+
+
+def source_flags(src):
+    """Per-file nvcc flags from `// nlk-build: <flags>` lines in the source
+    (e.g. a ptxas option measured better for the one kernel in that file)."""
+    flags = []
+    with open(src) as fh:
+        for line in fh:
+            if line.startswith("// nlk-build:"):
+                flags += line.split(":", 1)[1].split()
+    return flags
 
 
 def source_files():
@@ -103,7 +115,7 @@ def _build_id_object(obj_dir, defines):
     return obj
 
 
-def build(force=False, verbose=False, jobs=None, tag=None, defines=(), only=None):
+def build(force=False, verbose=False, jobs=None, tag=None, defines=(), only=None, xptxas=()):
     """Compile and link; ``tag``/``defines`` make a variant library
     ``libnlk_b200_<tag>.so`` (objects in ``_obj_<tag>``) for A/B timing.
     ``only`` (variants): recompile just the sources whose name contains one
@@ -114,12 +126,12 @@ def build(force=False, verbose=False, jobs=None, tag=None, defines=(), only=None
     jobs = jobs or os.cpu_count() or 4
     mine = [s for s in srcs if not only or any(k in os.path.basename(s) for k in only)]
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, defines), mine))
+        results = list(ex.map(lambda s: _compile(s, force, verbose, obj_dir, defines, xptxas), mine))
     objs = [o for o, _ in results]
     if only:  # the rest from the default build (must be current)
         objs += [os.path.join(OBJ, os.path.basename(s).replace(".cu", ".o")) for s in srcs
                  if s not in mine]
-    objs += [_build_id_object(obj_dir, list(defines))]
+    objs += [_build_id_object(obj_dir, list(defines) + [f"ptxas:{x}" for x in xptxas])]
     if (force or not os.path.exists(lib)
             or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
         cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, *objs]
@@ -138,8 +150,12 @@ def main(argv=None):
     ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for nvcc")
     ap.add_argument("--only", action="append", default=None,
                     help="variant: recompile only sources containing this substring")
+    ap.add_argument("--xptxas", action="append", default=[],
+                    help="variant: extra ptxas option (e.g. --register-usage-level=8)")
     a = ap.parse_args(argv)
-    print(build(a.force, a.verbose, a.jobs, a.tag, a.defines, a.only))
+    if (a.defines or a.xptxas) and not a.tag:
+        ap.error("-D / --xptxas build variants and need --tag")
+    print(build(a.force, a.verbose, a.jobs, a.tag, a.defines, a.only, a.xptxas))
 
 
 if __name__ == "__main__":
