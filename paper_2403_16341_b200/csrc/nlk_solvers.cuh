@@ -434,7 +434,13 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   // register-LU path the extra loop-carried state cost more than it saved
   // (matrix-sqrt-2x2 with a register LU: 36 -> 47 ms), so it keeps
   // dogleg_plain.
-  static constexpr bool kDlCache = SM && NLK_TR_DLCACHE;
+  // Round 2: below n = NLK_TR_DLCACHE_MIN_N the cache's loop-carried state
+  // costs more than the rejections it saves (matrix-sqrt-2x2 TR 29.4 -> 28.0
+  // ms without it; matrix-sqrt-3x3 TR 158.7 -> 166.9 ms and spills without it).
+#ifndef NLK_TR_DLCACHE_MIN_N
+#define NLK_TR_DLCACHE_MIN_N 5
+#endif
+  static constexpr bool kDlCache = SM && NLK_TR_DLCACHE && N >= NLK_TR_DLCACHE_MIN_N;
   T nnorm, gg, t_star, cnorm;
   int dl;
   NLK_FD void dogleg_cached(T* out) {
