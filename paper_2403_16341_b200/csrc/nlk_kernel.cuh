@@ -83,9 +83,17 @@ __device__ __forceinline__ void finish(const KernelArgs& a, const S& s, int st, 
   }
 }
 
-template <class P, int N, class T, int ALG>
+// Deferral (FAST kernels, below): a system the fast kernel cannot finish is
+// marked in its retcode slot (the stage's slot for a poly-algorithm stage)
+// and re-solved from its start by solve_kernel_deferred.
+constexpr int8_t kDeferMark = -2;
+__device__ __forceinline__ int8_t* defer_slot(const KernelArgs& a, int64_t sys) {
+  return a.poly_stage > 0 ? a.stage_rc + static_cast<int64_t>(a.poly_stage - 1) * a.B + sys : a.retcode + sys;
+}
+
+template <class P, int N, class T, int ALG, bool FAST = false>
 __global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solve_kernel(const KernelArgs a) {
-  using Solver = typename SolverOf<P, N, T, ALG>::type;
+  using Solver = typename SolverOf<P, N, T, ALG, FAST>::type;
   constexpr int M = P::M;
   const T* __restrict__ u0 = static_cast<const T*>(a.u0);
   const T* __restrict__ pp = static_cast<const T*>(a.p);
@@ -136,9 +144,43 @@ __global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solv
       st = s.step(abstol, a.maxiters);
     }
     if (st != RUNNING) {
-      finish<N>(a, s, st, sys, B, uo, ro);
+      if (FAST && st == DEFERRED) *defer_slot(a, sys) = kDeferMark;
+      else finish<N>(a, s, st, sys, B, uo, ro);
       sys = -1;
     }
+  }
+}
+
+// The systems a FAST kernel deferred, each solved from its start with the
+// complete solver (the dual-sweep fallback of a declined closed form inline):
+// the same operations on the same inputs as a complete kernel would have
+// run, so the outputs are the same bits.  Grid-stride over the marks; with
+// no deferred system it only reads the B mark bytes.
+template <class P, int N, class T, int ALG>
+__global__ void __launch_bounds__(block_of<P, N, T, ALG>(), NLK_MIN_BLOCKS) solve_kernel_deferred(const KernelArgs a) {
+  using Solver = typename SolverOf<P, N, T, ALG, false>::type;
+  constexpr int M = P::M;
+  const T* __restrict__ u0 = static_cast<const T*>(a.u0);
+  const T* __restrict__ pp = static_cast<const T*>(a.p);
+  T* __restrict__ uo = static_cast<T*>(a.u_out);
+  T* __restrict__ ro = static_cast<T*>(a.resid_out);
+  const T abstol = static_cast<T>(a.abstol);
+  const int64_t B = a.B;
+  Solver s;
+  if constexpr (Solver::kSmemElems > 0) {
+    extern __shared__ __align__(16) unsigned char nlk_dyn_smem[];
+    s.sm = reinterpret_cast<T*>(nlk_dyn_smem) + threadIdx.x;
+  }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t sys = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; sys < B; sys += stride) {
+    if (*defer_slot(a, sys) != kDeferMark) continue;
+#pragma unroll
+    for (int k = 0; k < N; ++k) s.u[k] = u0[k * B + sys];
+#pragma unroll
+    for (int k = 0; k < M; ++k) s.p[k] = pp[k * B + sys];
+    int st = s.init(abstol);
+    while (st == RUNNING) st = s.step(abstol, a.maxiters);
+    finish<N>(a, s, st, sys, B, uo, ro);
   }
 }
 
@@ -211,13 +253,26 @@ template <class P, int ALG> struct UseStatic {
   static constexpr bool value =
       NLK_SCHEDULE_STATIC_ALL || (NLK_SCHEDULE_STATIC && StaticSchedule<P, ALG>::value);
 };
+// NLK_FAST_DEFER: closed-form problems' Newton / trust-region kernels run
+// without the rarely-taken dual-sweep fallback and defer the systems that
+// need it (the fallback made the trigonometric trust region's kernel 1.6x
+// larger and 29 % slower: profiles/r02_variants.txt r02Z/r02AB)
+#ifndef NLK_FAST_DEFER
+#define NLK_FAST_DEFER 1
+#endif
+template <class P, int ALG, class T> struct UseFast {
+  static constexpr bool value = NLK_FAST_DEFER && HasJacClosedForm<P>::value && std::is_same<T, double>::value &&
+                                (ALG == ALG_NR || ALG == ALG_TR || ALG == ALG_NEWTON_LS) &&
+                                !UseStatic<P, ALG>::value;
+};
 
 // Host-side launcher: persistent grid sized from the occupancy calculator.
 template <class P, int N, class T, int ALG>
 cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out) {
+  constexpr bool kFast = UseFast<P, ALG, T>::value;
   auto kern = [] {
     if constexpr (UseStatic<P, ALG>::value) return solve_kernel_static<P, N, T, ALG>;
-    else return solve_kernel<P, N, T, ALG>;
+    else return solve_kernel<P, N, T, ALG, kFast>;
   }();
   constexpr int kThreads = block_of<P, N, T, ALG>();
   constexpr int per_block_systems = kThreads;
@@ -262,6 +317,19 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = static_cast<int>(grid);
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(a);
+  if constexpr (kFast) {
+    // the complete kernel for the deferred systems (same block and smem)
+    static thread_local bool attr_set[64];
+    if (!attr_set[dev] && smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(solve_kernel_deferred<P, N, T, ALG>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    attr_set[dev] = true;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    solve_kernel_deferred<P, N, T, ALG><<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(a);
+  }
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@
 namespace nlk {
 
 enum RetCode : int { SUCCESS = 0, MAXITERS = 1, LINESEARCH_FAILED = 2, LINSOLVE_FAILED = 3,
-                     STALLED = 4, NONFINITE = 5, RUNNING = -1 };
+                     STALLED = 4, NONFINITE = 5, RUNNING = -1, DEFERRED = -2 };
 enum Alg : int { ALG_NR = 0, ALG_TR = 1, ALG_BROYDEN = 2, ALG_KLEMENT = 3, ALG_DFSANE = 4,
                  ALG_NEWTON_LS = 5, NUM_ALGS = 6 };
 
@@ -173,13 +173,18 @@ struct HasJacClosedForm<P, std::void_t<decltype(P::kJacClosedForm)>> {
 #define NLK_JAC_CLOSED_FORM 1
 #endif
 
-template <class P, int N, class T, int KM, class JS>
+// FAST (the fast kernel of a closed-form problem, nlk_kernel.cuh): a
+// declined closed form returns kJacDefer instead of running the dual sweeps,
+// and the system is re-solved from its start by the complete kernel.
+constexpr int kJacDefer = -2;
+template <class P, int N, class T, int KM, bool FAST = false, class JS>
 NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
   if constexpr (NLK_JAC_CLOSED_FORM && HasJacClosedForm<P>::value && std::is_same<T, double>::value) {
     // memo = nullptr: the driver keeps no memo (the closed form evaluates
     // what it needs itself)
     if (P::jac_closed_form(u, KM > 0 ? memo : nullptr, [&](int e, T v) { jput(J, e, v); }))
       return -1;
+    if constexpr (FAST) return kJacDefer;
   }
   bool vals_ok = true;
   int bad_col = N;
@@ -194,7 +199,7 @@ NLK_FD int jacobian(const T* u, const T* p, T* memo, JS J) {
 // SCPAIRS: residuals evaluate their sincos in pairs per out-of-line call
 // (Ctx::sincos_all; measured faster for Newton, slower for the trust region,
 // whose extra live state then spills)
-template <class P, int N, class T, bool MEMO = true, bool SCPAIRS = false>
+template <class P, int N, class T, bool MEMO = true, bool SCPAIRS = false, bool FAST = false>
 struct Base {
   static constexpr int M = P::M;
   T u[N], f[N];
@@ -217,8 +222,9 @@ struct Base {
   // trust region re-evaluates J only after accepting u = ut right after F(ut).
   template <class JS>
   NLK_FD int jac(JS J) {
+    int bad = jacobian<P, N, T, KM, FAST>(u, p, memo, J);
+    if (FAST && bad == kJacDefer) return kJacDefer;
     njac += 1;
-    int bad = jacobian<P, N, T, KM>(u, p, memo, J);
     constexpr int chunks = (N + 7) / 8;
     nf += (bad < 0) ? chunks : bad + 1;
     return bad;
@@ -234,9 +240,9 @@ struct Base {
 };
 
 // ---- Newton-Raphson (optionally with backtracking line search) --------------
-template <class P, int N, class T, bool LS>
-struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
-  using B = Base<P, N, T, true, NLK_SINCOS_PAIRS_NR>;
+template <class P, int N, class T, bool LS, bool FAST = false>
+struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR, FAST> {
+  using B = Base<P, N, T, true, NLK_SINCOS_PAIRS_NR, FAST>;
   using SL = UseSmemLU<N, T, NLK_SMEM_NR_MIN>;
   static constexpr bool SM = SL::value;
   static constexpr int kSmemElems = SM ? N * N + N : 0;
@@ -250,7 +256,9 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
     T du[N];
     if constexpr (SM) {  // J streams column by column into the smem slice
       const Mat A{B::sm}, rhs{B::sm + N * N * kStride};
-      if (B::jac(A) >= 0) return NONFINITE;
+      const int jb = B::jac(A);
+      if (FAST && jb == kJacDefer) return DEFERRED;
+      if (jb >= 0) return NONFINITE;
       if constexpr (LS) {
 #pragma unroll
         for (int e = 0; e < N * N; ++e) Jf[e] = A.v(e);
@@ -264,7 +272,9 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
       for (int i = 0; i < N; ++i) du[i] = rhs.v(i);
     } else {
       T J[N * N];
-      if (B::jac(J) >= 0) return NONFINITE;
+      const int jb = B::jac(J);
+      if (FAST && jb == kJacDefer) return DEFERRED;
+      if (jb >= 0) return NONFINITE;
       if constexpr (LS) {
 #pragma unroll
         for (int i = 0; i < N * N; ++i) Jf[i] = J[i];
@@ -326,9 +336,9 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR> {
 #ifndef NLK_TR_FASTFWD
 #define NLK_TR_FASTFWD 1
 #endif
-template <class P, int N, class T>
-struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
-  using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR>;
+template <class P, int N, class T, bool FAST = false>
+struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR, FAST> {
+  using B = Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR, FAST>;
   using SL = UseSmemLU<N, T, NLK_SMEM_TR_MIN>;
   static constexpr bool SM = SL::value;
   static constexpr int kStride = SM ? SL::stride : kSmStride;
@@ -353,7 +363,11 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
   // f(J accessor); for RD the zero-sign lookups are skipped unless some
   // column value is zero
   template <class F> NLK_FD void with_j(F&& f) {
-    if constexpr (RD) {
+    if constexpr (RD && FAST) {
+      // only the closed form fills jrd here, and it declines whenever a
+      // column value would be zero: the zero-sign accessor is never needed
+      f(RDRef<N, T, false>{&jrd[0]});
+    } else if constexpr (RD) {
       if (jrd[0].zany) f(RDRef<N, T, true>{&jrd[0]});
       else f(RDRef<N, T, false>{&jrd[0]});
     } else {
@@ -518,7 +532,9 @@ struct TrustRegion : Base<P, N, T, NLK_TR_MEMO, NLK_SINCOS_PAIRS_TR> {
     if (!cached) {
       if constexpr (kDlCache) dl = 0;
       if constexpr (RD) jrd[0].reset();
-      if (B::jac(jmat()) >= 0) return NONFINITE;
+      const int jb = B::jac(jmat());
+      if (FAST && jb == kJacDefer) return DEFERRED;
+      if (jb >= 0) return NONFINITE;
       if constexpr (SM) {
         const Mat A{B::sm};
         with_j([&](auto Jm) {
@@ -851,13 +867,15 @@ struct DFSane : Base<P, N, T, false> {
   }
 };
 
-template <class P, int N, class T, int ALG> struct SolverOf;
-template <class P, int N, class T> struct SolverOf<P, N, T, ALG_NR> { using type = NewtonRaphson<P, N, T, false>; };
-template <class P, int N, class T> struct SolverOf<P, N, T, ALG_NEWTON_LS> { using type = NewtonRaphson<P, N, T, true>; };
-template <class P, int N, class T> struct SolverOf<P, N, T, ALG_TR> { using type = TrustRegion<P, N, T>; };
-template <class P, int N, class T> struct SolverOf<P, N, T, ALG_BROYDEN> { using type = QuasiNewton<P, N, T, false>; };
-template <class P, int N, class T> struct SolverOf<P, N, T, ALG_KLEMENT> { using type = QuasiNewton<P, N, T, true>; };
-template <class P, int N, class T> struct SolverOf<P, N, T, ALG_DFSANE> { using type = DFSane<P, N, T>; };
+// FAST: the fast variant of a closed-form problem's Newton / trust-region
+// solver (no dual-sweep fallback; see jacobian() and nlk_kernel.cuh)
+template <class P, int N, class T, int ALG, bool FAST = false> struct SolverOf;
+template <class P, int N, class T, bool F> struct SolverOf<P, N, T, ALG_NR, F> { using type = NewtonRaphson<P, N, T, false, F>; };
+template <class P, int N, class T, bool F> struct SolverOf<P, N, T, ALG_NEWTON_LS, F> { using type = NewtonRaphson<P, N, T, true, F>; };
+template <class P, int N, class T, bool F> struct SolverOf<P, N, T, ALG_TR, F> { using type = TrustRegion<P, N, T, F>; };
+template <class P, int N, class T, bool F> struct SolverOf<P, N, T, ALG_BROYDEN, F> { using type = QuasiNewton<P, N, T, false>; };
+template <class P, int N, class T, bool F> struct SolverOf<P, N, T, ALG_KLEMENT, F> { using type = QuasiNewton<P, N, T, true>; };
+template <class P, int N, class T, bool F> struct SolverOf<P, N, T, ALG_DFSANE, F> { using type = DFSane<P, N, T>; };
 
 #undef NLK_FD
 }  // namespace nlk
