@@ -538,6 +538,7 @@ struct MatrixSqrt2x2 {  // 213-220
 };
 struct MatrixSqrt3x3 {  // 223-230: R = X @ X - A
   static constexpr int N = 9, M = 0;
+  static constexpr bool kTrNoFastFwd = true;  // no radius-exhaustion tails (TrustRegion)
   // closed-form Jacobian: matsq_jac_closed_form (above)
   static constexpr bool kJacClosedForm = true;
   template <class T, class PUT>
