@@ -148,6 +148,12 @@ NLK_API int nlk_solve_batch_host_async(int32_t handle, int32_t alg, int32_t dtyp
  * (diagnostics for the persistent grid). */
 NLK_API int nlk_last_grid(void);
 
+/* Number of kernels the last nlk_solve_batch launch on this thread issued: 1,
+ * or 2 where a closed-form problem's fast Newton / trust-region kernel is
+ * followed by the kernel that completes its deferred systems (diagnostics;
+ * bench.py's gpu_launches). */
+NLK_API int nlk_last_launches(void);
+
 /* Measured FP64 FMA-pipe throughput of the current device in TFLOP/s (8
  * independent DFMA chains per thread, all SMs; synchronous on `stream`).
  * The roofline denominator for the solve kernels, which are FP64-issue

@@ -28,7 +28,7 @@ ERRORS = {
 # exported symbols, exactly those declared in include/nlk_b200.h
 SYMBOLS = ("nlk_version", "nlk_build_id", "nlk_last_error", "nlk_alg_lookup", "nlk_num_problems",
            "nlk_problem_info", "nlk_problem_lookup", "nlk_solve_batch",
-           "nlk_solve_batch_host", "nlk_solve_batch_host_async", "nlk_solve_batch_poly", "nlk_last_grid",
+           "nlk_solve_batch_host", "nlk_solve_batch_host_async", "nlk_solve_batch_poly", "nlk_last_grid", "nlk_last_launches",
            "nlk_fp64_peak", "nlk_fp32_peak", "nlk_ift_forward_batch", "nlk_ift_adjoint_batch")
 
 _lib = None
@@ -66,6 +66,7 @@ def lib():
     L.nlk_solve_batch_poly.argtypes = [i32, i32, i64, vp, vp, dbl, i32, vp, vp, vp, vp, vp, vp,
                                        vp, vp, vp]
     L.nlk_last_grid.restype = ctypes.c_int
+    L.nlk_last_launches.restype = ctypes.c_int
     L.nlk_fp64_peak.argtypes = [i64, ctypes.POINTER(dbl), vp]
     L.nlk_fp32_peak.argtypes = [i64, ctypes.POINTER(dbl), vp]
     L.nlk_ift_forward_batch.argtypes = [i32, i32, i64, vp, vp, dbl, vp, vp, vp, vp]

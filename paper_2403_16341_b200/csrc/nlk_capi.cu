@@ -175,6 +175,8 @@ const char* nlk_last_error(void) { return g_err.c_str(); }
 
 int nlk_last_grid(void) { return g_grid; }
 
+int nlk_last_launches(void) { return nlk::tl_launches(); }
+
 int nlk_alg_lookup(const char* name) {
   if (!name) return fail(NLK_ERR_UNKNOWN_ALG, "null algorithm name");
   for (int i = 0; i < nlk::NUM_ALGS; ++i)

@@ -266,6 +266,12 @@ template <class P, int ALG, class T> struct UseFast {
                                 !UseStatic<P, ALG>::value;
 };
 
+// kernels issued by the last launch_solve on this thread (nlk_last_launches)
+inline int& tl_launches() {
+  static thread_local int n = 0;
+  return n;
+}
+
 // Host-side launcher: persistent grid sized from the occupancy calculator.
 template <class P, int N, class T, int ALG>
 cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out) {
@@ -317,6 +323,7 @@ cudaError_t launch_solve(const KernelArgs& a, cudaStream_t stream, int* grid_out
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = static_cast<int>(grid);
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(a);
+  tl_launches() = kFast ? 2 : 1;
   if constexpr (kFast) {
     // the complete kernel for the deferred systems (same block and smem)
     static thread_local bool attr_set[64];
