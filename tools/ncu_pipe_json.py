@@ -32,7 +32,8 @@ def main(args):
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
     for rep, name, batch, match in zip(args[0::4], args[1::4], args[2::4], args[3::4]):
         for d in raw(rep):
-            if match not in d["Kernel Name"]:
+            # the solve kernel itself, not the one completing deferred systems
+            if match not in d["Kernel Name"] or "deferred" in d["Kernel Name"]:
                 continue
             e = {v: float(d[k]) for k, v in KEYS.items() if k in d}
             e["source"] = f"profiles/{os.path.basename(rep)} (ncu --set full, B = {batch})"
