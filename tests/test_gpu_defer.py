@@ -58,3 +58,28 @@ def test_deferred_systems_poly_match_oracle(pid, n):
     got = gpu_poly(pid, u0).to_numpy()
     check_poly_fields(ref, got, f"{pid} with deferred systems")
     assert (got["stage_retcodes"] >= -1).all()
+
+
+@pytest.mark.parametrize("alg_id,alg", [(0, "newton-raphson"), (1, "trust-region")])
+def test_deferred_systems_host_buffer_path(alg_id, alg):
+    """The host-buffer entry point (chunks staged over several streams): the
+    marks and the completion kernel work per chunk."""
+    import ctypes
+
+    from paper_2403_16341_b200 import _lib
+    pid, n = "test23/trigonometric", 10
+    u0 = _starts(pid, n, seed=31 + alg_id, B=9001)
+    ref = O.solve_batch(pid, alg, u0, None)
+    h, n_, _ = _lib.problem_lookup(pid, n)
+    B = len(u0)
+    u0s = np.ascontiguousarray(u0.T)
+    uo, ro = np.empty((n, B)), np.empty(B)
+    rc, cnt = np.empty(B, np.int8), np.empty((4, B), np.int32)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _lib.check(_lib.lib().nlk_solve_batch_host(h, alg_id, 0, B, ptr(u0s), None, 1e-8, 1000, ptr(uo),
+                                               ptr(ro), ptr(rc), ptr(cnt[0]), ptr(cnt[1]),
+                                               ptr(cnt[2]), ptr(cnt[3]), 2500, 3))
+    assert np.array_equal(rc, ref["retcode"])
+    for i, f in enumerate(("nsteps", "nf", "njac", "nlinsolve")):
+        assert np.array_equal(cnt[i], ref[f]), f
+    assert _same(uo.T, ref["u"]) and _same(ro, ref["resid"])
