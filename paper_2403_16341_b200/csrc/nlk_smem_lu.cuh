@@ -124,8 +124,8 @@ NLK_SMU
 
 // GETF2 on rows OFF..N-1, columns OFF..OFF+NC-1; piv holds absolute rows.
 // Returns the panel's interchanges composed (perm_* form).
-template <int N, class T, int S>
-NLK_FD uint64_t sm_getf2(const SMat<N, T, S>& A, int OFF, int NC, int* piv) {
+template <int N, class T, int S, class DV = ExactDiv>
+NLK_FD uint64_t sm_getf2(const SMat<N, T, S>& A, int OFF, int NC, int* piv, DV dv = DV{nullptr}) {
   const int M = N - OFF;
   uint64_t R = perm_identity<N>();
 NLK_SMU
@@ -219,7 +219,7 @@ NLK_SMU
 NLK_SMU
       for (int r = c + 1; r < N; ++r) outv[r] = (r == p) ? colv[c] : colv[r];
       if (fabs(pv) >= Num<T>::dbl_min) {
-        const T rr = T(1) / pv;
+        const T rr = dv(T(1), pv);
 NLK_SMU
         for (int r = c + 1; r < N; ++r) outv[r] = outv[r] * rr;
       }
@@ -242,7 +242,7 @@ NLK_SMU
       sm_swap_rows(A, c, p, OFF, c + 1);
       const T bj = A(c, c);
       if (fabs(bj) >= Num<T>::dbl_min) {
-        const T rr = T(1) / bj;
+        const T rr = dv(T(1), bj);
 NLK_SMU
         for (int r = c + 1; r < N; ++r) A(r, c) = A(r, c) * rr;
       }
@@ -289,18 +289,18 @@ NLK_SMU
   }
 }
 
-template <int N, class T, int S>
-NLK_FD void sm_getrf(const SMat<N, T, S>& A, int* piv) {
+template <int N, class T, int S, class DV = ExactDiv>
+NLK_FD void sm_getrf(const SMat<N, T, S>& A, int* piv, DV dv = DV{nullptr}) {
   constexpr int BLK = ((N / 2 + 1) / 2) * 2;
   if constexpr (BLK <= 4) {
-    sm_getf2(A, 0, N, piv);
+    sm_getf2(A, 0, N, piv, dv);
   } else {
     constexpr int NP = (N + BLK - 1) / BLK;
     uint64_t Rp[NP];  // each panel's interchanges, composed
 NLK_SMU
     for (int is = 0; is < N; is += BLK) {
       const int bk = (N - is) < BLK ? (N - is) : BLK;
-      Rp[is / BLK] = sm_getf2(A, is, bk, piv);  // panels of n <= 16 are always GETF2
+      Rp[is / BLK] = sm_getf2(A, is, bk, piv, dv);  // panels of n <= 16 are always GETF2
       if (is + bk < N) {
 #if NLK_LU_GATHER
 NLK_SMU
@@ -340,8 +340,8 @@ NLK_SMU
 // checks, so max|A| is finite and the scan below can only reject an all-zero
 // matrix -- which getrf rejects anyway (every pivot is zero), with the same
 // outcome (SingularMatrix -> LINSOLVE_FAILED).  The scan is skipped then.
-template <int N, bool JAC_CHECKED, class T, int S>
-NLK_FD bool sm_lu_factor(const SMat<N, T, S>& A, int* piv) {
+template <int N, bool JAC_CHECKED, class T, int S, class DV = ExactDiv>
+NLK_FD bool sm_lu_factor(const SMat<N, T, S>& A, int* piv, DV dv = DV{nullptr}) {
   if constexpr (!JAC_CHECKED) {
     T anorm = T(0);
     bool nan = false;
@@ -353,7 +353,7 @@ NLK_SMU
     }
     if (nan || anorm == T(0) || !isfinite(anorm)) return false;
   }
-  sm_getrf(A, piv);
+  sm_getrf(A, piv, dv);
   bool zero = false, pnan = false;
 NLK_SMU
   for (int i = 0; i < N; ++i) {
@@ -365,8 +365,8 @@ NLK_SMU
 }
 
 // getrs with the right-hand side in the strided vector b (N elements)
-template <int N, class T, int S>
-NLK_FD void sm_getrs(const SMat<N, T, S>& LU, const int* piv, const SMat<N, T, S>& b) {
+template <int N, class T, int S, class DV = ExactDiv>
+NLK_FD void sm_getrs(const SMat<N, T, S>& LU, const int* piv, const SMat<N, T, S>& b, DV dv = DV{nullptr}) {
 #if NLK_LU_GATHER
   {
     uint64_t R = perm_identity<N>();
@@ -399,7 +399,7 @@ NLK_SMU
   }
 NLK_SMU
   for (int i = N - 1; i >= 0; --i) {
-    x[i] = x[i] / LU(i, i);
+    x[i] = dv(x[i], LU(i, i));
 NLK_SMU
     for (int r = 0; r < i; ++r) x[r] = t_fma(-x[i], LU(r, i), x[r]);
   }
@@ -424,7 +424,7 @@ NLK_SMU
 #if NLK_GETRS_HOIST_DIV
     const T bi = div_with_rcp(b.v(i), LU(i, i), rd[i]);
 #else
-    const T bi = b.v(i) / LU(i, i);
+    const T bi = dv(b.v(i), LU(i, i));
 #endif
     b.v(i) = bi;
 NLK_SMU

@@ -229,9 +229,20 @@ struct Base {
     nf += (bad < 0) ? chunks : bad + 1;
     return bad;
   }
+  // FAST Newton: the LU's divisions take their inline fast path only
+  // (FlagDiv, nlk_div.cuh); dbad marks one outside it -> the step defers the
+  // system.  Measured: trig NR 162.6 -> 157.6 ms; the trust-region kernels
+  // were slower with it (trig TR 45.3 -> 48.6, msqrt-3x3 TR 154.1 -> 158.6)
+  // and keep `b / d`.
+  bool dbad;
+  NLK_FD auto divp() {
+    if constexpr (FAST) return FlagDiv{&dbad};
+    else return ExactDiv{nullptr};
+  }
   // shared prologue of every driver: f(u0), NONFINITE / already-converged
   NLK_FD int start(T abstol) {
     k = nsteps = nf = njac = nlinsolve = 0;
+    dbad = false;
     F(u, f);
     if (!all_finite<N>(f)) return NONFINITE;
     if (converged<N>(f, abstol)) return SUCCESS;
@@ -263,11 +274,15 @@ struct NewtonRaphson : Base<P, N, T, true, NLK_SINCOS_PAIRS_NR, FAST> {
 #pragma unroll
         for (int e = 0; e < N * N; ++e) Jf[e] = A.v(e);
       }
-      if (!sm_lu_factor<N, true>(A, piv)) return LINSOLVE_FAILED;
+      if (!sm_lu_factor<N, true>(A, piv, B::divp())) {
+        if (FAST && B::dbad) return DEFERRED;
+        return LINSOLVE_FAILED;
+      }
       B::nlinsolve += 1;
 #pragma unroll
       for (int i = 0; i < N; ++i) rhs.v(i) = -B::f[i];
-      sm_getrs<N>(A, piv, rhs);
+      sm_getrs<N>(A, piv, rhs, B::divp());
+      if (FAST && B::dbad) return DEFERRED;
 #pragma unroll
       for (int i = 0; i < N; ++i) du[i] = rhs.v(i);
     } else {

@@ -1,4 +1,4 @@
-// div_with_rcp(b, d, div_rcp(d)) and ddiv(b, d) against b / d, bit for bit
+// div_with_rcp(b, d, div_rcp(d)), ddiv(b, d) and FlagDiv against b / d, bit for bit
 // (see nlk_div.cuh).
 #include <cstdio>
 #include <cstdint>
@@ -44,6 +44,23 @@ __global__ void zerodiv(long long n, unsigned long long seed, double* out) {
     out[i] = nlk::ddiv(b, d);
   }
 }
+// FlagDiv (the fast Newton kernels' LU): where it does not flag, its result
+// must be b / d bit for bit; flagged operands take b / d here (the kernels
+// defer those systems instead)
+__global__ void flagged(long long n, unsigned long long seed, double* out, unsigned long long* nflag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t h1 = mix(seed + 2 * i), h2 = mix(seed + 2 * i + 1);
+    const double b = pick(mix(h1), static_cast<int>(h1 & 3)), d = pick(mix(h2), static_cast<int>((h1 >> 2) & 3));
+    bool bad = false;
+    double q = nlk::FlagDiv{&bad}(b, d);
+    if (bad) {
+      q = b / d;
+      atomicAdd(nflag, 1ull);
+    }
+    out[i] = q;
+  }
+}
 __global__ void plain(long long n, unsigned long long seed, double* out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -70,7 +87,9 @@ __global__ void compare(long long n, unsigned long long seed, const double* x, c
 }
 int main() {
   unsigned long long* bad; double *ex, *x, *y;
-  cudaMallocManaged(&bad, 8); cudaMallocManaged(&ex, 64);
+  unsigned long long* nflag;
+  cudaMallocManaged(&bad, 8); cudaMallocManaged(&ex, 64); cudaMallocManaged(&nflag, 8);
+  *nflag = 0;
   const long long chunk = 1ll << 25, total = 100000000;
   cudaMalloc(&x, chunk * 8); cudaMalloc(&y, chunk * 8);
   *bad = 0;
@@ -81,9 +100,11 @@ int main() {
     compare<<<148 * 8, 256>>>(chunk, seed, x, y, bad, ex);
     zerodiv<<<148 * 8, 256>>>(chunk, seed, x);
     compare<<<148 * 8, 256>>>(chunk, seed, x, y, bad, ex);
+    flagged<<<148 * 8, 256>>>(chunk, seed, x, nflag);
+    compare<<<148 * 8, 256>>>(chunk, seed, x, y, bad, ex);
   }
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("cuda error\n"); return 2; }
-  printf("checked %lld mismatches %llu\n", (total + chunk - 1) / chunk * chunk, *bad);
+  printf("checked %lld mismatches %llu (FlagDiv flagged %llu)\n", (total + chunk - 1) / chunk * chunk, *bad, *nflag);
   for (unsigned long long k = 0; k < *bad && k < 4; ++k) printf("  b=%a d=%a\n", ex[2 * k], ex[2 * k + 1]);
   return *bad ? 1 : 0;
 }

@@ -1,6 +1,7 @@
 """The divisions of paper_2403_16341_b200/csrc/nlk_div.cuh -- the
-hoisted-reciprocal division (div_with_rcp) and the zero-dividend shortcut
-used on the solve path (ddiv) -- are bit-identical to nvcc's `b / d` on 10^8
+hoisted-reciprocal division (div_with_rcp), the zero-dividend shortcut
+used on the solve path (ddiv) and the fast Newton kernels' flagged fast path
+(FlagDiv, wherever it does not flag) -- are bit-identical to nvcc's `b / d` on 10^8
 random operands (any bit pattern, moderate and extreme exponents, zeros,
 subnormals, infinities, NaN)."""
 
